@@ -1,0 +1,171 @@
+/*
+ * spotkm.h -- C ABI of the B200 (sm_100a) device-mapping / context-migration
+ * hot path of SpotServe (arXiv 2311.15566).
+ *
+ * The reference (`spotsim`, pure Python) exposes this path as Python
+ * functions; this ABI is what a Python/ctypes (or any FFI) binding calls in
+ * their place.  Each entry point below names the reference interface it
+ * replaces (file:line under /root/reference/pkg/src/spotsim/).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Pointers prefixed `d_` are DEVICE
+ *     pointers (caller-owned, e.g. torch tensors' data_ptr()); `h_` pointers
+ *     are host memory.  `stream` is a cudaStream_t passed as void*.
+ *   - All calls are asynchronous on `stream` and keep no global state; they
+ *     are re-entrant across distinct streams / buffers.
+ *   - Return value is an sk_status; sk_last_error() gives thread-local text.
+ *     Status -> reference exception: SK_EINVAL/SK_EGROUP -> MappingError,
+ *     SK_ENOSOURCE -> MigrationError, SK_ERANGE -> MappingError (inputs out
+ *     of the exact-arithmetic range), SK_ECUDA -> RuntimeError.
+ *
+ * Exactness contract: every edge weight is an exact integer
+ * numerator N over a per-plan denominator K (lcm of the tensor-shard counts),
+ * converted once with a correctly rounded division -- bit-identical to the
+ * reference's float(Fraction) (domain.py:299-320).  The matcher replays the
+ * reference's `_hungarian_max` (mapping.py:71-122) in IEEE double with the
+ * same operation order and tie-break, so assignments and total_weight are
+ * bit-identical.
+ */
+#ifndef SPOTKM_H
+#define SPOTKM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPOTKM_ABI_VERSION 1
+
+typedef enum {
+  SK_OK = 0,
+  SK_EINVAL = 1,    /* malformed arguments                       -> MappingError   */
+  SK_EGROUP = 2,    /* fused group does not divide G and M        -> MappingError   */
+  SK_ERANGE = 3,    /* numerator bound >= 2^53 (inexact)          -> MappingError   */
+  SK_ENOSOURCE = 4, /* a required shard has no live holder        -> MigrationError */
+  SK_ECUDA = 5,     /* CUDA runtime error                         -> RuntimeError   */
+  SK_ENOPEER = 6    /* peer access unavailable for the executor   -> RuntimeError   */
+} sk_status;
+
+/* plan flags */
+#define SK_PLAN_FUSED_SUM 1 /* fused edge weight = Python builtin sum() of the inner match (else max) */
+#define SK_PLAN_DENSE 2     /* the F buffer holds a caller-given dense W (km_match); no segments      */
+
+/*
+ * One context segment of an old GPU's inventory: layers [l0, l1) x the
+ * tensor-shard interval [a, b) / K.  pipe == 0: model parameters, `unit` =
+ * bytes_per_layer x multiplicity.  pipe >= 1: KV cache that counts only
+ * toward positions of NEW pipeline `pipe`; `unit` = kv_bytes_per_token_per_layer
+ * x sum over the segment's requests of min(tokens held, tokens needed).
+ * Shared bytes with position v = sum_seg |[l0,l1) & stage(v)| * |[a,b) & I(v)| * unit / K
+ * (the closed form of overlap_bytes, domain.py:299-320, on
+ * required_context_with_cache, mapping.py:155-169).
+ */
+typedef struct sk_segment {
+  int32_t l0, l1;
+  int32_t a, b;
+  int32_t pipe;
+  int32_t reserved;
+  int64_t unit;
+} sk_segment; /* 32 bytes */
+
+/*
+ * One mapping problem (one build_graph / map_devices call).
+ * Rows are the candidate GPUs in the reference row order (instances by
+ * natural_key, then local index; mapping.py:193-198); columns are the target
+ * positions in lexicographic (d, p, m) order (domain.py:92-99).
+ */
+typedef struct sk_plan {
+  int32_t rows;     /* R = candidate GPUs                                       */
+  int32_t D, P, M;  /* target configuration                                     */
+  int32_t L;        /* model layers                                             */
+  int32_t K;        /* common denominator of every interval (multiple of M)     */
+  int32_t group;    /* fused group size g = min(G, M) (1 = flat km_match)       */
+  int32_t flags;    /* SK_PLAN_*                                                */
+  int32_t row_base; /* row r's segments: seg[row_ptr[row_base+r] .. row_ptr[row_base+r+1]) */
+  int32_t reserved;
+  int64_t f_off;    /* element offset of the plan's fused matrix (nA x nB) and perm block */
+  int64_t out_off;  /* element offset of the plan's R assignment entries        */
+  int64_t reserved2;
+} sk_plan; /* 64 bytes */
+
+/* Library / ABI identification. */
+int sk_abi_version(void);
+const char* sk_last_error(void);
+
+/*
+ * K1 -- build_graph (mapping.py:184-216): dense W[R][C] in float64, one plan
+ * per call row block.  d_W receives, for plan q, R*C doubles at d_W + f_off.
+ */
+int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                     const sk_segment* d_segs, double* d_W, int max_rows, int max_cols,
+                     void* stream);
+
+/*
+ * K2 -- map_devices (mapping.py:222-283) for a batch of plans: per fused pair
+ * an inner KM on the g x g block (weights built on the fly, never stored),
+ * fused weight max|sum, then one warp per plan runs the outer KM on the
+ * zero-padded fused matrix and expands the assignment.  Also serves km_match
+ * (mapping.py:125-149) with group = 1.
+ *   d_fused : >= sum over plans of nA*nB doubles   (scratch, at f_off)
+ *   d_perm  : >= sum over plans of nA*nB uint32    (scratch, at f_off)
+ *   d_assign: per plan R int32 at out_off: column index or -1 (unassigned)
+ *   d_total : per plan total_weight (accumulated in the reference order)
+ *   max_pairs = max nA*nB, max_n = max(nA, nB), max_rows = max R over the batch.
+ *   group_mask: bit g set when some plan has group g (0 = any of 1..8).
+ */
+int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                   const sk_segment* d_segs, double* d_fused, uint32_t* d_perm,
+                   int32_t* d_assign, double* d_total, int64_t max_pairs, int max_n,
+                   int max_rows, int group_mask, void* stream);
+
+/*
+ * km_match on caller-given dense weights (mapping.py:125-149): plans with
+ * SK_PLAN_DENSE, group 1, W (R x C, row-major doubles) at d_W + f_off.
+ */
+int sk_km_dense(const sk_plan* d_plans, int n_plans, const double* d_W, int32_t* d_assign,
+                double* d_total, int max_n, int max_rows, void* stream);
+
+/*
+ * Sweep expansion: compact preemption-sweep descriptors -> sk_plan rows and
+ * segments on device (positional old layout on instances i-0..i-(n-1), alive
+ * subset, B cached requests per old pipeline with identity inheritance;
+ * SURVEY.md 8(d)).  Host precomputes offsets; the kernel writes row_ptr/segs.
+ */
+typedef struct sk_sweep_desc {
+  int32_t oD, oP, oM;    /* old configuration                        */
+  int32_t G;             /* GPUs per instance                        */
+  int32_t n_inst;        /* pool instances before preemption         */
+  int32_t alive_off;     /* word offset of the alive bitmask         */
+  int32_t tok_off;       /* offset of oD per-old-pipeline token sums */
+  int32_t plan;          /* index of the sk_plan this fills          */
+  int64_t bpl, kv;       /* model bytes per layer / kv per token per layer */
+} sk_sweep_desc; /* 48 bytes */
+
+int sk_sweep_expand(const sk_sweep_desc* d_desc, int n_desc, const uint32_t* d_alive,
+                    const int64_t* d_tok, const sk_plan* d_plans, int32_t* d_row_ptr,
+                    sk_segment* d_segs, int max_rows, void* stream);
+
+/*
+ * K3 -- migration executor (the paper's batched send/recv, PAPER.md:491-497;
+ * the reference only plans it: migration.py:311-384).  One byte-range copy
+ * per Transfer, pulled by the destination GPU from a peer-mapped source over
+ * NVLink.  Copies of one plan round run concurrently; `round_ptr` delimits
+ * rounds; copies are grouped per destination device.
+ */
+typedef struct sk_copy {
+  uint64_t src;   /* device address readable from the launching device (peer or local) */
+  uint64_t dst;   /* device address on the launching device                            */
+  uint64_t bytes;
+} sk_copy;
+
+int sk_copy_batched(const sk_copy* d_copies, int n_copies, int n_ctas, void* stream);
+
+/* Peer-access helper: enable access from `device` to each of `peers`. */
+int sk_enable_peer_access(int device, const int* peers, int n_peers);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPOTKM_H */

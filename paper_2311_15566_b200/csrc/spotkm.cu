@@ -1,0 +1,719 @@
+// spotkm.cu -- sm_100a kernels + C ABI for SpotServe's device-mapping and
+// context-migration hot path.  See include/spotkm.h for the contract and
+// DESIGN.md for the data layout and rooflines.
+//
+// Kernels
+//   k_weights      K1  dense W[R][C] (build_graph, mapping.py:184-216)
+//   k_fuse<g>      K2a per fused pair: g x g weight block built on the fly,
+//                      inner KM, fused weight (mapping.py:258-269)
+//   k_outer<CPL>   K2b one warp per plan: outer KM on the zero-padded fused
+//                      matrix (mapping.py:271, 71-122) + expansion and
+//                      total_weight in reference order (mapping.py:272-283)
+//   k_sweep_expand     compact sweep descriptors -> rows/segments
+//   k_copy         K3  byte-range copies (peer-mapped pull over NVLink)
+//
+// Exactness: no fast-math, -fmad=false.  Every float op of the reference's
+// _hungarian_max is replayed in the same order: cost = -w;
+// cur = (cost - u[i0]) - v[j]; strict '<' in the slack update and argmin with
+// the lowest column winning ties.
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/spotkm.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(SK_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return SK_OK;
+}
+
+constexpr double kInf = __builtin_huge_val();
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// context algebra on device
+
+struct Col {
+  int d;       // 1-based new pipeline
+  int s0, s1;  // stage layer block [s0, s1)           (domain.py:271-283)
+  int i0, i1;  // shard interval [i0, i1) in 1/K units (domain.py:286-288)
+};
+
+__device__ __forceinline__ Col col_of(const sk_plan& p, int c) {
+  const int m = c % p.M;
+  const int t = c / p.M;
+  const int st = t % p.P;
+  const int d = t / p.P;
+  const int q = p.L / p.P, r = p.L % p.P;
+  Col o;
+  o.d = d + 1;
+  o.s0 = st * q + min(st, r);
+  o.s1 = o.s0 + q + (st < r ? 1 : 0);
+  const int w = p.K / p.M;
+  o.i0 = m * w;
+  o.i1 = o.i0 + w;
+  return o;
+}
+
+__device__ __forceinline__ long long seg_num(const sk_segment& s, const Col& c) {
+  const int ol = min(s.l1, c.s1) - max(s.l0, c.s0);
+  const int oi = min(s.b, c.i1) - max(s.a, c.i0);
+  if (ol <= 0 || oi <= 0) return 0;
+  if (s.pipe != 0 && s.pipe != c.d) return 0;
+  return (long long)ol * (long long)oi * s.unit;
+}
+
+// N / K correctly rounded: exact N (< 2^53) and K, one IEEE division -- the
+// same value float(Fraction(N, K)) gives (domain.py:320).
+__device__ __forceinline__ double num_to_w(long long n, int K) {
+  return __ddiv_rn(__ll2double_rn(n), (double)K);
+}
+
+__device__ __forceinline__ double weight_at(const sk_plan& p, const int32_t* __restrict__ row_ptr,
+                                            const sk_segment* __restrict__ segs, int r, int c) {
+  const Col col = col_of(p, c);
+  const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
+  long long acc = 0;
+  for (int s = s0; s < s1; ++s) acc += seg_num(segs[s], col);
+  return num_to_w(acc, p.K);
+}
+
+// CPython >= 3.12 builtin sum() over floats with int start 0: the first item
+// goes through int + float, the rest through Neumaier compensation, and the
+// compensation is added once at the end when non-zero and finite
+// (mapping.py:268-269 fused_weight="sum"; SURVEY.md finding 6).
+template <int N>
+__device__ __forceinline__ double py_builtin_sum(const double (&x)[N]) {
+  double f = 0.0 + x[0];
+  double c = 0.0;
+#pragma unroll
+  for (int i = 1; i < N; ++i) {
+    const double xi = x[i];
+    const double t = f + xi;
+    if (fabs(f) >= fabs(xi))
+      c += (f - t) + xi;
+    else
+      c += (xi - t) + f;
+    f = t;
+  }
+  if (c != 0.0 && isfinite(c)) f += c;
+  return f;
+}
+
+// register-resident dynamic indexing for tiny arrays
+template <int N, typename T>
+__device__ __forceinline__ T sel(const T (&a)[N], int i) {
+  T r = a[0];
+#pragma unroll
+  for (int k = 1; k < N; ++k)
+    if (i == k) r = a[k];
+  return r;
+}
+template <int N, typename T>
+__device__ __forceinline__ void put(T (&a)[N], int i, T v) {
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+    if (i == k) a[k] = v;
+}
+
+// The reference _hungarian_max (mapping.py:71-122) on an N x N block held in
+// registers (N = fused group <= 8).  Returns perm[row] = column.
+template <int N>
+__device__ __forceinline__ void hungarian_small(const double (&w)[N][N], int (&perm)[N]) {
+  double u[N + 1], v[N + 1], minv[N + 1];
+  int match[N + 1], way[N + 1];
+  bool used[N + 1];
+#pragma unroll
+  for (int j = 0; j <= N; ++j) {
+    u[j] = 0.0;
+    v[j] = 0.0;
+    match[j] = 0;
+    way[j] = 0;
+  }
+  for (int i = 1; i <= N; ++i) {
+    match[0] = i;
+    int j0 = 0;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) {
+      minv[j] = kInf;
+      used[j] = false;
+    }
+    while (true) {
+      put(used, j0, true);
+      const int i0 = sel(match, j0);
+      const double ui0 = sel(u, i0);
+      double crow[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double x = w[0][j];
+#pragma unroll
+        for (int k = 1; k < N; ++k)
+          if (i0 - 1 == k) x = w[k][j];
+        crow[j] = -x;
+      }
+      double delta = kInf;
+      int j1 = 0;
+#pragma unroll
+      for (int j = 1; j <= N; ++j) {
+        if (!used[j]) {
+          const double cur = (crow[j - 1] - ui0) - v[j];
+          if (cur < minv[j]) {
+            minv[j] = cur;
+            way[j] = j0;
+          }
+          if (minv[j] < delta) {
+            delta = minv[j];
+            j1 = j;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j <= N; ++j) {
+        if (used[j]) {
+          const int r = match[j];
+#pragma unroll
+          for (int k = 0; k <= N; ++k)
+            if (k == r) u[k] += delta;
+          v[j] -= delta;
+        } else {
+          minv[j] -= delta;
+        }
+      }
+      j0 = j1;
+      if (sel(match, j0) == 0) break;
+    }
+    while (j0) {
+      const int j1 = sel(way, j0);
+      put(match, j0, sel(match, j1));
+      j0 = j1;
+    }
+  }
+#pragma unroll
+  for (int j = 1; j <= N; ++j) put(perm, match[j] - 1, j - 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1: dense weights, two adjacent columns per thread (16-B stores)
+
+constexpr int kW_TPB = 128;
+
+__global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ plans,
+                                                    const int32_t* __restrict__ row_ptr,
+                                                    const sk_segment* __restrict__ segs,
+                                                    double* __restrict__ W) {
+  const sk_plan p = plans[blockIdx.z];
+  const int r = blockIdx.y;
+  if (r >= p.rows) return;
+  const int C = p.D * p.P * p.M;
+  const int c = 2 * (blockIdx.x * kW_TPB + threadIdx.x);
+  if (c >= C) return;
+  const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
+  const Col ca = col_of(p, c);
+  const bool two = c + 1 < C;
+  const Col cb = two ? col_of(p, c + 1) : ca;
+  long long na = 0, nb = 0;
+  for (int s = s0; s < s1; ++s) {
+    const sk_segment sg = segs[s];
+    na += seg_num(sg, ca);
+    nb += seg_num(sg, cb);
+  }
+  double* out = W + p.f_off + (long long)r * C + c;
+  const double wa = num_to_w(na, p.K), wb = num_to_w(nb, p.K);
+  if (two && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    *reinterpret_cast<double2*>(out) = make_double2(wa, wb);
+  } else {
+    out[0] = wa;
+    if (two) out[1] = wb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2a: per fused pair (a, b): g x g block -> inner KM -> fused weight + perm
+
+constexpr int kF_TPB = 128;
+
+template <int G>
+__device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB,
+                                          const int32_t* __restrict__ row_ptr,
+                                          const sk_segment* __restrict__ segs,
+                                          double* __restrict__ F, uint32_t* __restrict__ perm_out) {
+  Col cols[G];
+#pragma unroll
+  for (int l = 0; l < G; ++l) cols[l] = col_of(p, b * G + l);
+  double w[G][G];
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    const int r = a * G + k;
+    const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
+    long long acc[G];
+#pragma unroll
+    for (int l = 0; l < G; ++l) acc[l] = 0;
+    for (int s = s0; s < s1; ++s) {
+      const sk_segment sg = segs[s];
+#pragma unroll
+      for (int l = 0; l < G; ++l) acc[l] += seg_num(sg, cols[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < G; ++l) w[k][l] = num_to_w(acc[l], p.K);
+  }
+  const long long idx = p.f_off + (long long)a * nB + b;
+  if (G == 1) {
+    F[idx] = w[0][0];  // max([w]) == sum([w]) == w for w >= 0
+    return;
+  }
+  int pm[G];
+  hungarian_small<G>(w, pm);
+  double picked[G];
+#pragma unroll
+  for (int k = 0; k < G; ++k) picked[k] = sel(w[k], pm[k]);
+  double f;
+  if (p.flags & SK_PLAN_FUSED_SUM) {
+    f = py_builtin_sum<G>(picked);
+  } else {
+    f = picked[0];
+#pragma unroll
+    for (int k = 1; k < G; ++k)
+      if (picked[k] > f) f = picked[k];
+  }
+  uint32_t packed = 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) packed |= (uint32_t)pm[k] << (4 * k);
+  F[idx] = f;
+  perm_out[idx] = packed;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
+                                                 const int32_t* __restrict__ row_ptr,
+                                                 const sk_segment* __restrict__ segs,
+                                                 double* __restrict__ F, uint32_t* __restrict__ perm) {
+  const sk_plan p = plans[plan0 + blockIdx.y];
+  if (p.group != G) return;
+  const int nA = p.rows / G;
+  const int nB = (p.D * p.P * p.M) / G;
+  const long long pair = (long long)blockIdx.x * kF_TPB + threadIdx.x;
+  if (pair >= (long long)nA * nB) return;
+  fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm);
+}
+
+template <int G>
+int launch_fuse(const sk_plan* d_plans, int p0, int np, long long max_pairs, const int32_t* row_ptr,
+                const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
+  const long long bx = (max_pairs + kF_TPB - 1) / kF_TPB;
+  dim3 grid((unsigned)bx, np);
+  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm);
+  return cuda_check("k_fuse launch");
+}
+
+// ---------------------------------------------------------------------------
+// K2b: outer KM, one warp per plan.  Column j is owned by lane j % 32 and its
+// slack (minv), potential v and used flag live in that lane's registers;
+// row potentials u, match and way live in shared memory.
+
+constexpr int kO_WARPS = 4;
+
+__host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows) {
+  return max_n + 1 > max_rows ? max_n + 1 : max_rows;
+}
+__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows) {
+  size_t bytes = (size_t)outer_dbl_elems(max_n, max_rows) * 8 + (size_t)(max_n + 1) * 4 * 2;
+  return (bytes + 15) & ~(size_t)15;
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restrict__ plans, int plan0, int n_plans,
+                                                         const int32_t* __restrict__ row_ptr,
+                                                         const sk_segment* __restrict__ segs,
+                                                         const double* __restrict__ F,
+                                                         const uint32_t* __restrict__ perm,
+                                                         int32_t* __restrict__ assign,
+                                                         double* __restrict__ total,
+                                                         size_t smem_per_warp, int max_n, int dbl_elems) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x * kO_WARPS + warp;
+  if (q >= n_plans) return;
+  const sk_plan p = plans[plan0 + q];
+  const int g = p.group;
+  const bool dense = (p.flags & SK_PLAN_DENSE) != 0;
+  const int C = p.D * p.P * p.M;
+  const int nA = p.rows / g, nB = C / g;
+  const int n = nA > nB ? nA : nB;
+
+  // per-warp layout: [double u/wv: dbl_elems] [int match: max_n+1] [int way: max_n+1]
+  unsigned char* base = smem + (size_t)warp * smem_per_warp;
+  const int n1 = max_n + 1;
+  double* u = reinterpret_cast<double*>(base);
+  int* match = reinterpret_cast<int*>(base + (size_t)dbl_elems * 8);
+  int* way = match + n1;
+
+  double v[CPL], minv[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) v[k] = 0.0;
+  for (int j = lane; j <= n; j += 32) {
+    u[j] = 0.0;
+    match[j] = 0;
+    way[j] = 0;
+  }
+  __syncwarp();
+
+  const double* Fp = F + p.f_off;
+  for (int i = 1; i <= n; ++i) {
+    if (lane == 0) match[0] = i;
+    unsigned long long used = 0ull;
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) minv[k] = kInf;
+    __syncwarp();
+    int j0 = 0;
+    while (true) {
+      if ((j0 & 31) == lane) used |= 1ull << (j0 >> 5);
+      const int i0 = match[j0];
+      const double ui0 = u[i0];
+      const bool row_real = (i0 - 1) < nA;
+      const double* rowp = Fp + (long long)(i0 - 1) * nB;
+      // gather this step's cost row (independent loads, MLP = CPL)
+      double cst[CPL];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int j = lane + 32 * k;
+        double x = 0.0;
+        if (row_real && j >= 1 && j <= nB && !((used >> k) & 1ull)) x = __ldg(rowp + (j - 1));
+        cst[k] = -x;
+      }
+      double best = kInf;
+      int bj = 0x7fffffff;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int j = lane + 32 * k;
+        if (j >= 1 && j <= n && !((used >> k) & 1ull)) {
+          const double cur = (cst[k] - ui0) - v[k];
+          if (cur < minv[k]) {
+            minv[k] = cur;
+            way[j] = j0;
+          }
+          if (minv[k] < best) {
+            best = minv[k];
+            bj = j;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double ob = __shfl_xor_sync(kFull, best, off);
+        const int oj = __shfl_xor_sync(kFull, bj, off);
+        if (ob < best || (ob == best && oj < bj)) {
+          best = ob;
+          bj = oj;
+        }
+      }
+      const double delta = best;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int j = lane + 32 * k;
+        if (j <= n) {
+          if ((used >> k) & 1ull) {
+            u[match[j]] += delta;
+            v[k] -= delta;
+          } else {
+            minv[k] -= delta;
+          }
+        }
+      }
+      __syncwarp();
+      j0 = bj;
+      if (match[j0] == 0) break;
+    }
+    if (lane == 0) {
+      while (j0) {
+        const int j1 = way[j0];
+        match[j0] = match[j1];
+        j0 = j1;
+      }
+    }
+    __syncwarp();
+  }
+
+  // row_to_col for real fused rows -> way[] (free now)
+  for (int j = lane + 1; j <= n; j += 32) {
+    const int r = match[j];
+    if (r >= 1 && r <= nA) way[r - 1] = j - 1;
+  }
+  __syncwarp();
+  double* wv = u;
+  int32_t* out = assign + p.out_off;
+  for (int r = lane; r < p.rows; r += 32) {
+    const int a = r / g, k = r % g;
+    const int b = way[a];
+    if (b < nB) {
+      int col = b * g;
+      if (g > 1) col += (int)((perm[p.f_off + (long long)a * nB + b] >> (4 * k)) & 15u);
+      const double w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
+      out[r] = col;
+      wv[r] = w;
+    } else {
+      out[r] = -1;
+      wv[r] = -1.0;
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double t = 0.0;
+    for (int r = 0; r < p.rows; ++r) {
+      const double w = wv[r];
+      if (w >= 0.0) t += w;
+    }
+    total[plan0 + q] = t;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sweep expansion: compact descriptors -> rows x 2 segments (model + cache)
+
+__global__ void k_sweep_expand(const sk_sweep_desc* __restrict__ desc, const uint32_t* __restrict__ alive,
+                               const int64_t* __restrict__ tok, const sk_plan* __restrict__ plans,
+                               int32_t* __restrict__ row_ptr, sk_segment* __restrict__ segs) {
+  const sk_sweep_desc ds = desc[blockIdx.y];
+  const sk_plan p = plans[ds.plan];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p.rows) return;
+  const int G = ds.G;
+  const int rank = r / G, g = r % G;
+  // index of the rank-th alive instance (instances i-0..i-(n-1) in natural order)
+  const int words = (ds.n_inst + 31) >> 5;
+  int k = -1, seen = 0;
+  for (int w = 0; w < words; ++w) {
+    const uint32_t bits = alive[ds.alive_off + w];
+    const int c = __popc(bits);
+    if (seen + c > rank) {
+      uint32_t b = bits;
+      for (int t = rank - seen; t > 0; --t) b &= b - 1;
+      k = w * 32 + __ffs(b) - 1;
+      break;
+    }
+    seen += c;
+  }
+  const long long x = (long long)p.row_base + r;
+  if (r == 0) row_ptr[p.row_base] = (int32_t)(2 * (long long)p.row_base);
+  row_ptr[x + 1] = (int32_t)(2 * (x + 1));
+  sk_segment ms = {0, 0, 0, 0, 0, 0, 0};
+  sk_segment cs = {0, 0, 0, 0, 0, 0, 0};
+  const int q = k * G + g;
+  if (k >= 0 && q < ds.oD * ds.oP * ds.oM) {
+    const int m = q % ds.oM, st = (q / ds.oM) % ds.oP, d = q / (ds.oM * ds.oP);
+    const int qq = p.L / ds.oP, rr = p.L % ds.oP;
+    const int s0 = st * qq + min(st, rr);
+    const int s1 = s0 + qq + (st < rr ? 1 : 0);
+    const int w = p.K / ds.oM;
+    ms.l0 = s0;
+    ms.l1 = s1;
+    ms.a = m * w;
+    ms.b = m * w + w;
+    ms.pipe = 0;
+    ms.unit = ds.bpl;
+    const long long tsum = tok[ds.tok_off + d];
+    if (tsum > 0 && d + 1 <= p.D) {  // identity inheritance on min(D_old, D_new)
+      cs = ms;
+      cs.pipe = d + 1;
+      cs.unit = ds.kv * tsum;
+    }
+  }
+  segs[2 * x] = ms;
+  segs[2 * x + 1] = cs;
+}
+
+// ---------------------------------------------------------------------------
+// K3: batched byte-range copies (the executor's data path).  Each CTA walks
+// whole chunks; 16-B vector loads from the (peer-mapped) source with 4
+// independent requests in flight per thread.
+
+constexpr int kC_TPB = 512;
+
+__global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ copies, int n) {
+  for (int c = blockIdx.x; c < n; c += gridDim.x) {
+    const sk_copy cp = copies[c];
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(cp.src);
+    unsigned char* dst = reinterpret_cast<unsigned char*>(cp.dst);
+    const uint64_t bytes = cp.bytes;
+    const bool aligned = ((cp.src | cp.dst) & 15ull) == 0;
+    uint64_t done = 0;
+    if (aligned) {
+      const uint64_t nv = bytes >> 4;
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+      int4* d4 = reinterpret_cast<int4*>(dst);
+      uint64_t i = threadIdx.x;
+      constexpr int U = 4;
+      for (; i + (U - 1) * kC_TPB < nv; i += U * kC_TPB) {
+        int4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = __ldcs(s4 + i + u * kC_TPB);
+#pragma unroll
+        for (int u = 0; u < U; ++u) __stcs(d4 + i + u * kC_TPB, t[u]);
+      }
+      for (; i < nv; i += kC_TPB) __stcs(d4 + i, __ldcs(s4 + i));
+      done = nv << 4;
+    }
+    for (uint64_t i = done + threadIdx.x; i < bytes; i += kC_TPB) dst[i] = src[i];
+  }
+}
+
+template <int CPL>
+int launch_outer(const sk_plan* d_plans, int plan0, int n_plans, const int32_t* row_ptr,
+                 const sk_segment* segs, const double* F, const uint32_t* perm, int32_t* assign,
+                 double* total, int max_n, int max_rows, cudaStream_t s) {
+  const size_t per_warp = outer_smem_per_warp(max_n, max_rows);
+  const size_t smem = per_warp * kO_WARPS;
+  if (smem > 227 * 1024) return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", smem);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_outer<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = true;
+  }
+  const int blocks = (n_plans + kO_WARPS - 1) / kO_WARPS;
+  k_outer<CPL><<<blocks, kO_WARPS * 32, smem, s>>>(d_plans, plan0, n_plans, row_ptr, segs, F, perm,
+                                                   assign, total, per_warp, max_n,
+                                                   outer_dbl_elems(max_n, max_rows));
+  return cuda_check("k_outer launch");
+}
+
+int outer_dispatch(const sk_plan* d_plans, int plan0, int n_plans, const int32_t* row_ptr,
+                   const sk_segment* segs, const double* F, const uint32_t* perm, int32_t* assign,
+                   double* total, int max_n, int max_rows, cudaStream_t s) {
+  const int need = max_n + 1;
+  if (need <= 32) return launch_outer<1>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 64) return launch_outer<2>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 128) return launch_outer<4>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 256) return launch_outer<8>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 512) return launch_outer<16>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 32 * 33) return launch_outer<33>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  if (need <= 32 * 64) return launch_outer<64>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
+  return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", max_n);
+}
+
+constexpr int kMaxGridY = 65535;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int sk_abi_version(void) { return SPOTKM_ABI_VERSION; }
+
+const char* sk_last_error(void) { return g_err; }
+
+int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                     const sk_segment* d_segs, double* d_W, int max_rows, int max_cols, void* stream) {
+  if (n_plans < 0 || max_rows < 0 || max_cols < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0 || max_rows == 0 || max_cols == 0) return SK_OK;
+  if (max_rows > kMaxGridY) return set_err(SK_EINVAL, "rows %d > %d", max_rows, kMaxGridY);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
+    const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
+    dim3 grid((max_cols + 2 * kW_TPB - 1) / (2 * kW_TPB), max_rows, np);
+    k_weights<<<grid, kW_TPB, 0, s>>>(d_plans + p0, d_row_ptr, d_segs, d_W);
+    int rc = cuda_check("k_weights launch");
+    if (rc) return rc;
+  }
+  return SK_OK;
+}
+
+int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                   const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int32_t* d_assign,
+                   double* d_total, int64_t max_pairs, int max_n, int max_rows, int group_mask,
+                   void* stream) {
+  if (n_plans < 0 || max_pairs < 0 || max_n < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0) return SK_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
+    const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
+    if (max_pairs > 0) {
+      if ((max_pairs + kF_TPB - 1) / kF_TPB > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
+      const int mask = group_mask ? group_mask : 0x1fe;
+      int rc = SK_OK;
+      if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 4))) rc = launch_fuse<4>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 5))) rc = launch_fuse<5>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 6))) rc = launch_fuse<6>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 7))) rc = launch_fuse<7>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (!rc && (mask & (1 << 8))) rc = launch_fuse<8>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+      if (rc) return rc;
+    }
+  }
+  return outer_dispatch(d_plans, 0, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total,
+                        max_n, max_rows, s);
+}
+
+int sk_km_dense(const sk_plan* d_plans, int n_plans, const double* d_W, int32_t* d_assign,
+                double* d_total, int max_n, int max_rows, void* stream) {
+  if (n_plans < 0 || max_n < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0) return SK_OK;
+  return outer_dispatch(d_plans, 0, n_plans, nullptr, nullptr, d_W, nullptr, d_assign, d_total,
+                        max_n, max_rows, static_cast<cudaStream_t>(stream));
+}
+
+int sk_sweep_expand(const sk_sweep_desc* d_desc, int n_desc, const uint32_t* d_alive,
+                    const int64_t* d_tok, const sk_plan* d_plans, int32_t* d_row_ptr,
+                    sk_segment* d_segs, int max_rows, void* stream) {
+  if (n_desc < 0 || max_rows < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_desc == 0 || max_rows == 0) return SK_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int p0 = 0; p0 < n_desc; p0 += kMaxGridY) {
+    const int np = n_desc - p0 < kMaxGridY ? n_desc - p0 : kMaxGridY;
+    dim3 grid((max_rows + 127) / 128, np);
+    k_sweep_expand<<<grid, 128, 0, s>>>(d_desc + p0, d_alive, d_tok, d_plans, d_row_ptr, d_segs);
+    int rc = cuda_check("k_sweep_expand launch");
+    if (rc) return rc;
+  }
+  return SK_OK;
+}
+
+int sk_copy_batched(const sk_copy* d_copies, int n_copies, int n_ctas, void* stream) {
+  if (n_copies < 0) return set_err(SK_EINVAL, "negative copy count");
+  if (n_copies == 0) return SK_OK;
+  if (n_ctas <= 0) n_ctas = 148 * 4;
+  k_copy<<<n_ctas, kC_TPB, 0, static_cast<cudaStream_t>(stream)>>>(d_copies, n_copies);
+  return cuda_check("k_copy launch");
+}
+
+int sk_enable_peer_access(int device, const int* peers, int n_peers) {
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(device) != cudaSuccess) return set_err(SK_ECUDA, "cudaSetDevice(%d)", device);
+  for (int i = 0; i < n_peers; ++i) {
+    if (peers[i] == device) continue;
+    int ok = 0;
+    cudaDeviceCanAccessPeer(&ok, device, peers[i]);
+    if (!ok) {
+      cudaSetDevice(prev);
+      return set_err(SK_ENOPEER, "device %d cannot access peer %d", device, peers[i]);
+    }
+    cudaError_t e = cudaDeviceEnablePeerAccess(peers[i], 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+      cudaSetDevice(prev);
+      return set_err(SK_ECUDA, "enable peer %d->%d: %s", device, peers[i], cudaGetErrorString(e));
+    }
+    cudaGetLastError();
+  }
+  cudaSetDevice(prev);
+  return SK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+"""Host packer: GPU context inventories -> exact integer segments (sk_segment).
+
+A row's inventory (model shards (layer, lo, hi) and cache shards (rid, layer,
+lo, hi, tokens), reference domain.py:175-220) is rewritten over one common
+denominator K as runs of consecutive layers sharing an interval:
+
+* model runs   (l0, l1, a, b, pipe=0, unit = bytes_per_layer * multiplicity)
+* cache runs   (l0, l1, a, b, pipe=d, unit = kv * sum_r min(tokens_held, tokens_needed))
+  where d is the NEW pipeline whose positions need request r's cache
+  (required_context_with_cache, mapping.py:155-169, fed by the inheritance
+  map, mapping.py:200-208).
+
+Then the reference's exact overlap (domain.py:299-320) between row u and
+position v equals  sum_seg |[l0,l1) & stage(v)| * |[a,b) & I(v)| * unit / K,
+which the device evaluates in int64 and converts with one correctly rounded
+division.  Nothing here computes a weight; it only re-encodes inventories.
+"""
+
+from __future__ import annotations
+
+from math import lcm
+
+import numpy as np
+
+from ._native import SEGMENT
+
+EXACT_LIMIT = 1 << 53
+K_LIMIT = (1 << 31) - 1
+
+
+class PackError(ValueError):
+    pass
+
+
+def _den(x) -> int:
+    return x.denominator
+
+
+def common_denominator(inventories, tensor_shards: int) -> int:
+    dens = {tensor_shards}
+    for inv in inventories:
+        for _, lo, hi in inv.model_shards:
+            dens.add(lo.denominator)
+            dens.add(hi.denominator)
+        for _, _, lo, hi, _ in inv.cache_shards:
+            dens.add(lo.denominator)
+            dens.add(hi.denominator)
+    K = 1
+    for d in dens:
+        K = lcm(K, d)
+    if K > K_LIMIT:
+        raise PackError(f"common interval denominator {K} exceeds 2^31-1")
+    return K
+
+
+def inherited_by_new(inheritance, requests_by_old_pipeline):
+    """new pipeline -> [(rid, tokens)], old pipelines ascending, requests by id
+    (mapping.py:200-208)."""
+    out: dict[int, list] = {}
+    if inheritance and requests_by_old_pipeline:
+        for d_old in sorted(requests_by_old_pipeline):
+            d_new = inheritance.get(d_old)
+            if d_new is None:
+                continue
+            for req in sorted(requests_by_old_pipeline[d_old], key=lambda r: r.id):
+                out.setdefault(d_new, []).append((req.id, req.s_in + req.tokens_generated))
+    return out
+
+
+def need_tokens(inherited: dict) -> dict:
+    """rid -> [(new pipeline, tokens)] for tokens > 0 (the filter of
+    mapping.py:167)."""
+    out: dict[str, list] = {}
+    for d_new in sorted(inherited):
+        for rid, tok in inherited[d_new]:
+            if tok > 0:
+                out.setdefault(rid, []).append((d_new, tok))
+    return out
+
+
+def _runs(entries):
+    """entries: {(key..., layer): unit}; merge consecutive layers with equal
+    (key, unit) -> [(l0, l1, key, unit)]."""
+    out = []
+    for k in sorted(entries):
+        *key, layer = k
+        unit = entries[k]
+        key = tuple(key)
+        if out and out[-1][2] == key and out[-1][3] == unit and out[-1][1] == layer:
+            l0, _, kk, uu = out[-1]
+            out[-1] = (l0, layer + 1, kk, uu)
+        else:
+            out.append((layer, layer + 1, key, unit))
+    return out
+
+
+def pack_row(inv, K: int, bpl: int, kv: int, need: dict):
+    """One inventory -> list of (l0, l1, a, b, pipe, unit)."""
+    scale: dict = {}
+
+    def num(x):
+        r = scale.get(x)
+        if r is None:
+            r = x.numerator * (K // x.denominator)
+            scale[x] = r
+        return r
+
+    model: dict = {}
+    for layer, lo, hi in inv.model_shards:
+        k = (num(lo), num(hi), layer)
+        model[k] = model.get(k, 0) + 1
+    segs = [(l0, l1, a, b, 0, bpl * mult) for l0, l1, (a, b), mult in _runs(model)]
+    if need and inv.cache_shards:
+        cache: dict = {}
+        for rid, layer, lo, hi, tok in inv.cache_shards:
+            ents = need.get(rid)
+            if not ents:
+                continue
+            a, b = num(lo), num(hi)
+            for d_new, t in ents:
+                k = (a, b, d_new, layer)
+                cache[k] = cache.get(k, 0) + (tok if tok < t else t)
+        segs.extend((l0, l1, a, b, d, kv * tsum) for l0, l1, (a, b, d), tsum in _runs(cache) if tsum)
+    return segs
+
+
+def pack_rows(inventories, K: int, bpl: int, kv: int, need: dict):
+    """-> (row_ptr int32[R+1], segments SEGMENT[S])."""
+    rows = [pack_row(inv, K, bpl, kv, need) for inv in inventories]
+    row_ptr = np.zeros(len(rows) + 1, dtype=np.int32)
+    total = 0
+    for i, segs in enumerate(rows):
+        # every W numerator of this row is <= the sum of its segments' spans
+        if sum((s[1] - s[0]) * (s[3] - s[2]) * s[5] for s in segs) >= EXACT_LIMIT:
+            raise PackError("edge-weight numerator may exceed 2^53: outside the exact range")
+        total += len(segs)
+        row_ptr[i + 1] = total
+    out = np.zeros(total, dtype=SEGMENT)
+    if total:
+        arr = np.array([s for segs in rows for s in segs], dtype=np.int64)
+        for f, col in (("l0", 0), ("l1", 1), ("a", 2), ("b", 3), ("pipe", 4)):
+            out[f] = arr[:, col]
+        out["unit"] = arr[:, 5]
+    return row_ptr, out

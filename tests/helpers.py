@@ -1,0 +1,37 @@
+"""Test helpers: golden cases -> this package's own domain objects."""
+
+from __future__ import annotations
+
+from cases import decode_map_case
+
+import paper_2311_15566_b200 as sk
+from paper_2311_15566_b200.domain import natural_key
+
+
+def own_problem(case):
+    model, target, G, instances, inh, reqs, fw = decode_map_case(case)
+    mspec = sk.ModelSpec(name="m", num_layers=model[0], bytes_per_layer=model[1],
+                         kv_bytes_per_token_per_layer=model[2])
+    cfg = sk.ParallelConfig(*target, 1)
+    insts = []
+    for iid, invs in instances:
+        insts.append(sk.InstanceState(
+            id=iid, kind="spot", gpus=len(invs),
+            gpu_inventories=[sk.ContextInventory(model_shards=inv.model, cache_shards=inv.cache)
+                             for inv in invs]))
+    rq = None
+    if reqs is not None:
+        rq = {d: [sk.RequestSpec(id=rid, arrival_time=0.0, s_in=tok, s_out=max(tok, 1))
+                  for rid, tok in lst] for d, lst in reqs.items()}
+    return mspec, cfg, G, insts, inh, rq, fw
+
+
+def assignment_cols(mapping, instances, cfg):
+    slots = sk.positions(cfg)
+    col = {s: j for j, s in enumerate(slots)}
+    out = []
+    for inst in sorted(instances, key=lambda i: natural_key(i.id)):
+        for g in range(inst.gpus):
+            pos = mapping.assignment.get((inst.id, g))
+            out.append(-1 if pos is None else col[pos])
+    return out

@@ -1,0 +1,55 @@
+"""Pin the CPU oracle (oracle/port.py) to the reference's own outputs.
+
+The golden files were produced by running the real `spotsim` reference
+(tests/golden/gen_golden.py).  Everything here is bit-exact: W entries,
+assignments and total weights compare as float hex.
+"""
+
+import pytest
+
+from cases import decode_map_case, golden_w
+from fmt import unhx
+from oracle import port
+
+
+def test_km_cases_bit_exact(golden):
+    doc = golden("km")
+    assert len(doc["cases"]) > 400
+    for case in doc["cases"]:
+        W = [[unhx(x) for x in row] for row in case["W"]]
+        n_r, n_c = len(W), len(W[0])
+        n = max(n_r, n_c)
+        assert port.hungarian_max(port.pad_square(W)) == case["perm"]
+        assign, total = port.km_flat(W, n_r, n_c)
+        assert assign == case["assign"]
+        assert total.hex() == case["total"]
+        assert n >= 1
+
+
+@pytest.mark.parametrize("name", ["mapping", "scenario"])
+def test_mapping_cases_bit_exact(golden, name):
+    doc = golden(name)
+    cases = doc["cases"] if name == "mapping" else doc["maps"]
+    n_checked = 0
+    for case in cases:
+        model, target, G, instances, inh, reqs, fw = decode_map_case(case)
+        if "W" in case:
+            _, _, W = port.build_weights(instances, target, model, inh, reqs)
+            assert [[x.hex() for x in row] for row in W] == case["W"]
+        if case["error"]:
+            with pytest.raises(port.OracleError):
+                port.map_devices(instances, target, model, G, inh, reqs, fw)
+            continue
+        _, _, W, assign, total = port.map_devices(instances, target, model, G, inh, reqs, fw)
+        assert assign == case["assign"]
+        assert total.hex() == case["total"]
+        n_checked += 1
+    assert n_checked >= 10
+
+
+def test_tie_break_is_not_lexicographic(golden):
+    """SURVEY finding 4: the reference's answer on this tie-heavy matrix is not
+    the lexicographically least optimum; the oracle must reproduce it."""
+    W = [[0.0, 0.0, 2.0, 0.0], [1.0, 0.0, 1.0, 1.0], [0.0, 0.0, 2.0, 0.0], [0.0, 0.0, 0.0, 1.0]]
+    assert port.hungarian_max(W) == [2, 0, 1, 3]
+    _ = golden_w
