@@ -119,6 +119,18 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
                    int32_t* d_assign, double* d_total, int64_t max_pairs, int max_n,
                    int max_rows, int group_mask, void* stream);
 
+/* The two halves of sk_map_batched, for callers that time or pipeline them:
+ * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  d_steps
+ * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element
+ * loads} (2 x int64) -- the algorithmic work of the outer KM. */
+int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int64_t max_pairs,
+                int group_mask, void* stream);
+int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                 const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                 int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                 void* stream);
+
 /*
  * km_match on caller-given dense weights (mapping.py:125-149): plans with
  * SK_PLAN_DENSE, group 1, W (R x C, row-major doubles) at d_W + f_off.

@@ -35,7 +35,8 @@ COPY = np.dtype([("src", "<u8"), ("dst", "<u8"), ("bytes", "<u8")], align=True)
 assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize == 48 and COPY.itemsize == 24
 
 EXPORTS = (
-    "sk_abi_version", "sk_last_error", "sk_build_weights", "sk_map_batched", "sk_km_dense",
+    "sk_abi_version", "sk_last_error", "sk_build_weights", "sk_map_batched", "sk_map_fuse",
+    "sk_map_outer", "sk_km_dense",
     "sk_sweep_expand", "sk_copy_batched", "sk_enable_peer_access",
 )
 
@@ -68,6 +69,8 @@ def load():
         "sk_last_error": ([], ctypes.c_char_p),
         "sk_build_weights": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
         "sk_map_batched": ([vp, i32, vp, vp, vp, vp, vp, vp, i64, i32, i32, i32, vp], i32),
+        "sk_map_fuse": ([vp, i32, vp, vp, vp, vp, i64, i32, vp], i32),
+        "sk_map_outer": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], i32),
         "sk_km_dense": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),
         "sk_copy_batched": ([vp, i32, i32, vp], i32),

@@ -335,20 +335,32 @@ __host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int ma
   return (bytes + 15) & ~(size_t)15;
 }
 
+struct OuterArgs {
+  const sk_plan* plans;
+  int n_plans;
+  const int32_t* row_ptr;
+  const sk_segment* segs;
+  const double* F;
+  const uint32_t* perm;
+  int32_t* assign;
+  double* total;
+  int64_t* steps;  // optional: Dijkstra steps per plan (profiling)
+  size_t smem_per_warp;
+  int max_n;
+  int dbl_elems;
+};
+
 template <int CPL>
-__global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restrict__ plans, int plan0, int n_plans,
-                                                         const int32_t* __restrict__ row_ptr,
-                                                         const sk_segment* __restrict__ segs,
-                                                         const double* __restrict__ F,
-                                                         const uint32_t* __restrict__ perm,
-                                                         int32_t* __restrict__ assign,
-                                                         double* __restrict__ total,
-                                                         size_t smem_per_warp, int max_n, int dbl_elems) {
+__global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = blockIdx.x * kO_WARPS + warp;
-  if (q >= n_plans) return;
-  const sk_plan p = plans[plan0 + q];
+  if (q >= A.n_plans) return;
+  const sk_plan p = A.plans[q];
+  const int32_t* __restrict__ row_ptr = A.row_ptr;
+  const sk_segment* __restrict__ segs = A.segs;
+  const uint32_t* __restrict__ perm = A.perm;
+  const int max_n = A.max_n;
   const int g = p.group;
   const bool dense = (p.flags & SK_PLAN_DENSE) != 0;
   const int C = p.D * p.P * p.M;
@@ -356,10 +368,10 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
   const int n = nA > nB ? nA : nB;
 
   // per-warp layout: [double u/wv: dbl_elems] [int match: max_n+1] [int way: max_n+1]
-  unsigned char* base = smem + (size_t)warp * smem_per_warp;
+  unsigned char* base = smem + (size_t)warp * A.smem_per_warp;
   const int n1 = max_n + 1;
   double* u = reinterpret_cast<double*>(base);
-  int* match = reinterpret_cast<int*>(base + (size_t)dbl_elems * 8);
+  int* match = reinterpret_cast<int*>(base + (size_t)A.dbl_elems * 8);
   int* way = match + n1;
 
   double v[CPL], minv[CPL];
@@ -372,7 +384,8 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
   }
   __syncwarp();
 
-  const double* Fp = F + p.f_off;
+  const double* Fp = A.F + p.f_off;
+  long long nsteps = 0, nloads = 0;
   for (int i = 1; i <= n; ++i) {
     if (lane == 0) match[0] = i;
     unsigned long long used = 0ull;
@@ -381,6 +394,7 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
     __syncwarp();
     int j0 = 0;
     while (true) {
+      ++nsteps;
       if ((j0 & 31) == lane) used |= 1ull << (j0 >> 5);
       const int i0 = match[j0];
       const double ui0 = u[i0];
@@ -392,7 +406,10 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
       for (int k = 0; k < CPL; ++k) {
         const int j = lane + 32 * k;
         double x = 0.0;
-        if (row_real && j >= 1 && j <= nB && !((used >> k) & 1ull)) x = __ldg(rowp + (j - 1));
+        if (row_real && j >= 1 && j <= nB && !((used >> k) & 1ull)) {
+          x = __ldg(rowp + (j - 1));
+          ++nloads;
+        }
         cst[k] = -x;
       }
       double best = kInf;
@@ -455,7 +472,7 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
   }
   __syncwarp();
   double* wv = u;
-  int32_t* out = assign + p.out_off;
+  int32_t* out = A.assign + p.out_off;
   for (int r = lane; r < p.rows; r += 32) {
     const int a = r / g, k = r % g;
     const int b = way[a];
@@ -471,13 +488,19 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const sk_plan* __restri
     }
   }
   __syncwarp();
+  if (A.steps) {
+#pragma unroll
+    for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);
+    if (lane == 0) A.steps[2 * q + 1] = nloads;
+  }
   if (lane == 0) {
     double t = 0.0;
     for (int r = 0; r < p.rows; ++r) {
       const double w = wv[r];
       if (w >= 0.0) t += w;
     }
-    total[plan0 + q] = t;
+    A.total[q] = t;
+    if (A.steps) A.steps[2 * q] = nsteps;
   }
 }
 
@@ -572,36 +595,31 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
 }
 
 template <int CPL>
-int launch_outer(const sk_plan* d_plans, int plan0, int n_plans, const int32_t* row_ptr,
-                 const sk_segment* segs, const double* F, const uint32_t* perm, int32_t* assign,
-                 double* total, int max_n, int max_rows, cudaStream_t s) {
-  const size_t per_warp = outer_smem_per_warp(max_n, max_rows);
-  const size_t smem = per_warp * kO_WARPS;
+int launch_outer(OuterArgs A, int max_rows, cudaStream_t s) {
+  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows);
+  A.dbl_elems = outer_dbl_elems(A.max_n, max_rows);
+  const size_t smem = A.smem_per_warp * kO_WARPS;
   if (smem > 227 * 1024) return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", smem);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_outer<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  const int blocks = (n_plans + kO_WARPS - 1) / kO_WARPS;
-  k_outer<CPL><<<blocks, kO_WARPS * 32, smem, s>>>(d_plans, plan0, n_plans, row_ptr, segs, F, perm,
-                                                   assign, total, per_warp, max_n,
-                                                   outer_dbl_elems(max_n, max_rows));
+  const int blocks = (A.n_plans + kO_WARPS - 1) / kO_WARPS;
+  k_outer<CPL><<<blocks, kO_WARPS * 32, smem, s>>>(A);
   return cuda_check("k_outer launch");
 }
 
-int outer_dispatch(const sk_plan* d_plans, int plan0, int n_plans, const int32_t* row_ptr,
-                   const sk_segment* segs, const double* F, const uint32_t* perm, int32_t* assign,
-                   double* total, int max_n, int max_rows, cudaStream_t s) {
-  const int need = max_n + 1;
-  if (need <= 32) return launch_outer<1>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 64) return launch_outer<2>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 128) return launch_outer<4>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 256) return launch_outer<8>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 512) return launch_outer<16>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 32 * 33) return launch_outer<33>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  if (need <= 32 * 64) return launch_outer<64>(d_plans, plan0, n_plans, row_ptr, segs, F, perm, assign, total, max_n, max_rows, s);
-  return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", max_n);
+int outer_dispatch(const OuterArgs& A, int max_rows, cudaStream_t s) {
+  const int need = A.max_n + 1;
+  if (need <= 32) return launch_outer<1>(A, max_rows, s);
+  if (need <= 64) return launch_outer<2>(A, max_rows, s);
+  if (need <= 128) return launch_outer<4>(A, max_rows, s);
+  if (need <= 256) return launch_outer<8>(A, max_rows, s);
+  if (need <= 512) return launch_outer<16>(A, max_rows, s);
+  if (need <= 32 * 33) return launch_outer<33>(A, max_rows, s);
+  if (need <= 32 * 64) return launch_outer<64>(A, max_rows, s);
+  return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", A.max_n);
 }
 
 constexpr int kMaxGridY = 65535;
@@ -633,40 +651,54 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
   return SK_OK;
 }
 
+int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int64_t max_pairs,
+                int group_mask, void* stream) {
+  if (n_plans < 0 || max_pairs < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0 || max_pairs == 0) return SK_OK;
+  if ((max_pairs + kF_TPB - 1) / kF_TPB > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int mask = group_mask ? group_mask : 0x1fe;
+  for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
+    const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
+    int rc = SK_OK;
+    if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 4))) rc = launch_fuse<4>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 5))) rc = launch_fuse<5>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 6))) rc = launch_fuse<6>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 7))) rc = launch_fuse<7>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 8))) rc = launch_fuse<8>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (rc) return rc;
+  }
+  return SK_OK;
+}
+
+int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                 const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                 int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                 void* stream) {
+  if (n_plans < 0 || max_n < 0 || max_rows < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0) return SK_OK;
+  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, 0, max_n, 0};
+  return outer_dispatch(A, max_rows, static_cast<cudaStream_t>(stream));
+}
+
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int32_t* d_assign,
                    double* d_total, int64_t max_pairs, int max_n, int max_rows, int group_mask,
                    void* stream) {
-  if (n_plans < 0 || max_pairs < 0 || max_n < 0) return set_err(SK_EINVAL, "negative sizes");
-  if (n_plans == 0) return SK_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
-    const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
-    if (max_pairs > 0) {
-      if ((max_pairs + kF_TPB - 1) / kF_TPB > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
-      const int mask = group_mask ? group_mask : 0x1fe;
-      int rc = SK_OK;
-      if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 4))) rc = launch_fuse<4>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 5))) rc = launch_fuse<5>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 6))) rc = launch_fuse<6>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 7))) rc = launch_fuse<7>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (!rc && (mask & (1 << 8))) rc = launch_fuse<8>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-      if (rc) return rc;
-    }
-  }
-  return outer_dispatch(d_plans, 0, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total,
-                        max_n, max_rows, s);
+  int rc = sk_map_fuse(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, max_pairs, group_mask, stream);
+  if (rc) return rc;
+  return sk_map_outer(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, nullptr,
+                      max_n, max_rows, stream);
 }
 
 int sk_km_dense(const sk_plan* d_plans, int n_plans, const double* d_W, int32_t* d_assign,
                 double* d_total, int max_n, int max_rows, void* stream) {
-  if (n_plans < 0 || max_n < 0) return set_err(SK_EINVAL, "negative sizes");
-  if (n_plans == 0) return SK_OK;
-  return outer_dispatch(d_plans, 0, n_plans, nullptr, nullptr, d_W, nullptr, d_assign, d_total,
-                        max_n, max_rows, static_cast<cudaStream_t>(stream));
+  return sk_map_outer(d_plans, n_plans, nullptr, nullptr, d_W, nullptr, d_assign, d_total, nullptr,
+                      max_n, max_rows, stream);
 }
 
 int sk_sweep_expand(const sk_sweep_desc* d_desc, int n_desc, const uint32_t* d_alive,

@@ -1,0 +1,225 @@
+"""Batched preemption sweep: many device-mapping plans per device call.
+
+This is the batched GPU entry point of the mapping path:
+for one target size N, every (old, new) pair of candidate (D,P,M) configs
+x S random preemption sets.  A plan is described compactly (sk_sweep_desc:
+old config, pool size, an alive-instance bitmask, per-old-pipeline cached
+token sums); `sk_sweep_expand` turns it into rows/segments on the device and
+`sk_map_batched` solves it.  Host -> device traffic per plan is ~0.2 KB;
+device -> host is the assignment (4 B per GPU row) + total_weight.
+
+Synthetic-input semantics: instances i-0..i-(n-1) with
+n = ceil(max(old, new GPUs) / G) + 4; the old config laid out positionally on
+them; k ~ U{1..4} instances preempted (without replacement); each old
+pipeline carries `batch` cached requests of 512 + U{0..128} tokens; identity
+inheritance on min(D_old, D_new).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from math import lcm
+
+import numpy as np
+import torch
+
+from . import _native as nat
+
+# (L, bytes_per_layer, kv_bytes_per_token_per_layer) from the reference profiles
+GPT20B = (44, 1693181818, 24576)      # data/profile_gpt20b.json:3-7
+LLAMA30B = (60, 1863333333, 26624)    # data/profile_llama30b.json:3-7
+OPT67B = (32, 781250000, 16384)       # data/profile_opt67b.json:3-7
+# candidate (P, M) shapes = the profiles' t_dec keys
+GPT20B_SHAPES = ((2, 8), (3, 4), (4, 4), (4, 8), (6, 2), (6, 4))
+LLAMA30B_SHAPES = ((2, 8), (4, 4), (4, 8), (8, 2))
+OPT67B_SHAPES = ((1, 4), (2, 2), (2, 4), (4, 2))
+MODELS = {"gpt-20b": (GPT20B, GPT20B_SHAPES), "llama-30b": (LLAMA30B, LLAMA30B_SHAPES),
+          "opt-6.7b": (OPT67B, OPT67B_SHAPES)}
+
+
+def sweep_configs(n_positions: int, shapes=GPT20B_SHAPES):
+    return [(n_positions // (P * M), P, M) for P, M in shapes if n_positions // (P * M) >= 1]
+
+
+@dataclass
+class SweepBatch:
+    """Host arrays of one batch of sweep plans (all numpy, ready for one H2D)."""
+
+    desc: np.ndarray    # SWEEP_DESC[Q]
+    plans: np.ndarray   # PLAN[Q]
+    alive: np.ndarray   # uint32 bitmask words
+    tok: np.ndarray     # int64 per old pipeline token sums
+    n_positions: int
+
+    @property
+    def n_plans(self) -> int:
+        return len(self.plans)
+
+    @property
+    def rows(self) -> int:
+        return int(self.plans["rows"].sum())
+
+    def stats(self):
+        g = self.plans["group"].astype(np.int64)
+        R = self.plans["rows"].astype(np.int64)
+        C = (self.plans["D"] * self.plans["P"] * self.plans["M"]).astype(np.int64)
+        nA, nB = R // g, C // g
+        return dict(rows=R, cols=C, nA=nA, nB=nB, n=np.maximum(nA, nB), pairs=nA * nB)
+
+
+def make_sweep(n_positions: int, sets_per_pair: int, seed: int = 0, G: int = 4, batch: int = 4,
+               model=GPT20B, shapes=GPT20B_SHAPES, fused_sum: bool = False,
+               pairs=None) -> SweepBatch:
+    """All (old, new) config pairs x `sets_per_pair` preemption sets."""
+    rng = np.random.default_rng(seed)
+    cfgs = sweep_configs(n_positions, shapes)
+    if pairs is None:
+        pairs = [(o, n) for o in cfgs for n in cfgs]
+    L, bpl, kv = model
+    descs, plans, alive_parts, tok_parts = [], [], [], []
+    alive_off = tok_off = 0
+    for old, new in pairs:
+        oD, oP, oM = old
+        nD, nP, nM = new
+        S = sets_per_pair
+        n_inst = -(-max(oD * oP * oM, nD * nP * nM) // G) + 4
+        k = rng.integers(1, 5, size=S)
+        ranks = rng.random((S, n_inst)).argsort(axis=1).argsort(axis=1)
+        alive = ranks >= k[:, None]                            # drop k instances
+        words = (n_inst + 31) // 32
+        bits = np.zeros((S, words * 32), dtype=bool)
+        bits[:, :n_inst] = alive
+        packed = np.packbits(bits.reshape(S, words, 32), axis=2, bitorder="little")
+        alive_w = packed.reshape(S, words * 4).view(np.uint32).reshape(S, words)
+        toks = rng.integers(512, 641, size=(S, oD, batch)).sum(axis=2).astype(np.int64)
+        rows = alive.sum(axis=1).astype(np.int64) * G
+        group = min(G, nM)
+        K = lcm(oM, nM)
+        d = np.zeros(S, dtype=nat.SWEEP_DESC)
+        d["oD"], d["oP"], d["oM"], d["G"], d["n_inst"] = oD, oP, oM, G, n_inst
+        d["alive_off"] = alive_off + np.arange(S) * words
+        d["tok_off"] = tok_off + np.arange(S) * oD
+        d["bpl"], d["kv"] = bpl, kv
+        p = np.zeros(S, dtype=nat.PLAN)
+        p["rows"], p["D"], p["P"], p["M"], p["L"], p["K"] = rows, nD, nP, nM, L, K
+        p["group"] = group
+        p["flags"] = nat.SK_PLAN_FUSED_SUM if fused_sum else 0
+        descs.append(d)
+        plans.append(p)
+        alive_parts.append(alive_w.reshape(-1))
+        tok_parts.append(toks.reshape(-1))
+        alive_off += S * words
+        tok_off += S * oD
+    desc = np.concatenate(descs)
+    plan = np.concatenate(plans)
+    desc["plan"] = np.arange(len(plan))
+    R = plan["rows"].astype(np.int64)
+    g = plan["group"].astype(np.int64)
+    C = (plan["D"] * plan["P"] * plan["M"]).astype(np.int64)
+    pairs_n = (R // g) * (C // g)
+    plan["row_base"] = np.concatenate([[0], np.cumsum(R)[:-1]])
+    plan["out_off"] = plan["row_base"]
+    plan["f_off"] = np.concatenate([[0], np.cumsum(pairs_n)[:-1]])
+    if R.sum() * 2 >= 2**31:
+        raise ValueError("sweep batch too large for int32 segment indices; split it")
+    return SweepBatch(desc, plan, np.concatenate(alive_parts).astype(np.uint32),
+                      np.concatenate(tok_parts).astype(np.int64), n_positions)
+
+
+def _align(n: int, a: int = 256) -> int:
+    return (n + a - 1) // a * a
+
+
+class SweepRunner:
+    """Device buffers for one SweepBatch; `run()` = one pass of the hot path.
+
+    Inputs live in one pinned host buffer and one device buffer; `upload()`
+    is the H2D step, `solve()` the kernels (expand + fused inner KM + outer
+    KM), `download()` the D2H of assignments and totals.
+    """
+
+    def __init__(self, batch: SweepBatch, device=None, stream=None):
+        self.lib = nat.load()
+        self.b = batch
+        self.dev = torch.device(device or "cuda")
+        st = batch.stats()
+        self.max_pairs = int(st["pairs"].max())
+        self.max_n = int(st["n"].max())
+        self.max_rows = int(st["rows"].max())
+        self.gmask = int(np.bitwise_or.reduce(1 << batch.plans["group"].astype(np.int64)))
+        parts = [batch.desc, batch.plans, batch.alive, batch.tok]
+        self.offs, total = [], 0
+        for a in parts:
+            self.offs.append(total)
+            total = _align(total + a.nbytes)
+        self.h_in = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+        hv = self.h_in.numpy()
+        for a, o in zip(parts, self.offs):
+            hv[o:o + a.nbytes] = np.frombuffer(a.tobytes(), dtype=np.uint8)
+        self.h2d_bytes = total
+        self.d_in = torch.empty(total, dtype=torch.uint8, device=self.dev)
+        R = batch.rows
+        Q = batch.n_plans
+        self.row_ptr = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
+        self.segs = torch.empty(2 * R * 32, dtype=torch.uint8, device=self.dev)
+        pairs = int(st["pairs"].sum())
+        self.fused = torch.empty(max(pairs, 1), dtype=torch.float64, device=self.dev)
+        self.perm = torch.empty(max(pairs, 1), dtype=torch.int32, device=self.dev)
+        self.out_bytes = _align(8 * Q + 4 * R)
+        self.d_out = torch.empty(self.out_bytes, dtype=torch.uint8, device=self.dev)
+        self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8, pin_memory=True)
+        self.d2h_bytes = 8 * Q + 4 * R
+        self.stream = stream
+
+    def _s(self) -> int:
+        return (self.stream or torch.cuda.current_stream(self.dev)).cuda_stream
+
+    def upload(self):
+        self.d_in.copy_(self.h_in, non_blocking=True)
+
+    def solve(self, marks=None, steps=None):
+        """Expand + fused inner KM + outer KM on the runner's stream.
+        marks: optional list of 4 torch.cuda.Event recorded at the phase
+        boundaries (expand | fuse | outer); steps: optional int64 device tensor
+        [2*Q] receiving {Dijkstra steps, cost loads} per plan."""
+        base = self.d_in.data_ptr()
+        p_desc, p_plans, p_alive, p_tok = (base + o for o in self.offs)
+        Q = self.b.n_plans
+        st = self._s()
+        if marks:
+            marks[0].record()
+        rc = self.lib.sk_sweep_expand(p_desc, Q, p_alive, p_tok, p_plans, self.row_ptr.data_ptr(),
+                                      self.segs.data_ptr(), self.max_rows, st)
+        nat.check(rc)
+        if marks:
+            marks[1].record()
+        rc = self.lib.sk_map_fuse(p_plans, Q, self.row_ptr.data_ptr(), self.segs.data_ptr(),
+                                  self.fused.data_ptr(), self.perm.data_ptr(), self.max_pairs,
+                                  self.gmask, st)
+        nat.check(rc)
+        if marks:
+            marks[2].record()
+        out = self.d_out.data_ptr()
+        rc = self.lib.sk_map_outer(p_plans, Q, self.row_ptr.data_ptr(), self.segs.data_ptr(),
+                                   self.fused.data_ptr(), self.perm.data_ptr(), out + 8 * Q, out,
+                                   0 if steps is None else steps.data_ptr(), self.max_n,
+                                   self.max_rows, st)
+        nat.check(rc)
+        if marks:
+            marks[3].record()
+
+    def download(self):
+        self.h_out.copy_(self.d_out, non_blocking=True)
+
+    def results(self):
+        """(assign int32[sum R], totals float64[Q]) -- call after synchronize."""
+        h = self.h_out.numpy()
+        Q, R = self.b.n_plans, self.b.rows
+        return h[8 * Q:8 * Q + 4 * R].view(np.int32).copy(), h[:8 * Q].view(np.float64).copy()
+
+    def run(self):
+        self.upload()
+        self.solve()
+        self.download()
+        torch.cuda.current_stream(self.dev).synchronize()
+        return self.results()
