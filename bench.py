@@ -99,7 +99,8 @@ class Clocks:
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[4 + i]})
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[4 + i].strip() == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.rows)}
@@ -313,7 +314,7 @@ def run_ours(args):
     batch = sweep.make_sweep(args.positions, args.sets, seed=1000 + rank, model=geom, shapes=shapes)
     runner = sweep.SweepRunner(batch)
     n_groups = bin(runner.gmask).count("1")
-    per_step_launches = 1 + n_groups + 1
+    per_step_launches = 1 + n_groups + len(runner.classes)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     K, W = args.steps, args.warmup
     dev_ms, e2e_ms, phase, clk, launches = measure_ours(runner, K, W, world, rank, local, flush,
@@ -387,7 +388,7 @@ def run_ours(args):
     if args.all_sizes:
         sizes = {}
         for n_pos in (64, 128, 256, 512, 1024):
-            sets = max(1, args.sets * 256 // n_pos) if n_pos < 1024 else max(1, args.sets // 8)
+            sets = {64: 256, 128: 256, 256: 256, 512: 64, 1024: 32}[n_pos]
             b = sweep.make_sweep(n_pos, sets, seed=2000 + rank, model=geom, shapes=shapes)
             r = sweep.SweepRunner(b)
             d_ms, x_ms, ph, _, _ = measure_ours(r, max(2, K // 2), 2, world, rank, local, flush,

@@ -117,7 +117,7 @@ __device__ __forceinline__ double py_builtin_sum(const double (&x)[N]) {
 
 // register-resident dynamic indexing for tiny arrays
 template <int N, typename T>
-__device__ __forceinline__ T sel(const T (&a)[N], int i) {
+__host__ __device__ __forceinline__ T sel(const T (&a)[N], int i) {
   T r = a[0];
 #pragma unroll
   for (int k = 1; k < N; ++k)
@@ -125,7 +125,7 @@ __device__ __forceinline__ T sel(const T (&a)[N], int i) {
   return r;
 }
 template <int N, typename T>
-__device__ __forceinline__ void put(T (&a)[N], int i, T v) {
+__host__ __device__ __forceinline__ void put(T (&a)[N], int i, T v) {
 #pragma unroll
   for (int k = 0; k < N; ++k)
     if (i == k) a[k] = v;
@@ -134,7 +134,7 @@ __device__ __forceinline__ void put(T (&a)[N], int i, T v) {
 // The reference _hungarian_max (mapping.py:71-122) on an N x N block held in
 // registers (N = fused group <= 8).  Returns perm[row] = column.
 template <int N>
-__device__ __forceinline__ void hungarian_small(const double (&w)[N][N], int (&perm)[N]) {
+__host__ __device__ __forceinline__ void hungarian_small(const double (&w)[N][N], int (&perm)[N]) {
   double u[N + 1], v[N + 1], minv[N + 1];
   int match[N + 1], way[N + 1];
   bool used[N + 1];
@@ -251,27 +251,51 @@ template <int G>
 __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB,
                                           const int32_t* __restrict__ row_ptr,
                                           const sk_segment* __restrict__ segs,
-                                          double* __restrict__ F, uint32_t* __restrict__ perm_out) {
-  Col cols[G];
-#pragma unroll
-  for (int l = 0; l < G; ++l) cols[l] = col_of(p, b * G + l);
-  double w[G][G];
+                                          double* __restrict__ F, uint32_t* __restrict__ perm_out,
+                                          uint32_t zero_perm) {
+  // the G columns of fused slot b share (pipeline, stage): one decode
+  const Col c0 = col_of(p, b * G);
+  const int wdt = c0.i1 - c0.i0;
+  long long num[G][G];
+  long long any = 0;
 #pragma unroll
   for (int k = 0; k < G; ++k) {
     const int r = a * G + k;
     const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
-    long long acc[G];
 #pragma unroll
-    for (int l = 0; l < G; ++l) acc[l] = 0;
+    for (int l = 0; l < G; ++l) num[k][l] = 0;
     for (int s = s0; s < s1; ++s) {
       const sk_segment sg = segs[s];
+      const int ol = min(sg.l1, c0.s1) - max(sg.l0, c0.s0);
+      if (ol <= 0 || (sg.pipe != 0 && sg.pipe != c0.d)) continue;
+      const long long per = (long long)ol * sg.unit;
 #pragma unroll
-      for (int l = 0; l < G; ++l) acc[l] += seg_num(sg, cols[l]);
+      for (int l = 0; l < G; ++l) {
+        const int oi = min(sg.b, c0.i0 + (l + 1) * wdt) - max(sg.a, c0.i0 + l * wdt);
+        if (oi > 0) num[k][l] += per * oi;
+      }
     }
 #pragma unroll
-    for (int l = 0; l < G; ++l) w[k][l] = num_to_w(acc[l], p.K);
+    for (int l = 0; l < G; ++l) any |= num[k][l];
   }
   const long long idx = p.f_off + (long long)a * nB + b;
+  if (any == 0) {
+    // all-zero block: max / builtin sum of zeros are 0.0 and the inner KM's
+    // answer is the (replayed) zero-matrix permutation
+    F[idx] = 0.0;
+    if (G > 1) perm_out[idx] = zero_perm;
+    return;
+  }
+  // N / K: exact reciprocal multiply when K is a power of two (bit-identical
+  // to the correctly rounded division), else the IEEE division
+  const bool pow2 = (p.K & (p.K - 1)) == 0;
+  const double inv = 1.0 / (double)p.K;
+  double w[G][G];
+#pragma unroll
+  for (int k = 0; k < G; ++k)
+#pragma unroll
+    for (int l = 0; l < G; ++l)
+      w[k][l] = pow2 ? __ll2double_rn(num[k][l]) * inv : num_to_w(num[k][l], p.K);
   if (G == 1) {
     F[idx] = w[0][0];  // max([w]) == sum([w]) == w for w >= 0
     return;
@@ -301,38 +325,80 @@ template <int G>
 __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
                                                  const int32_t* __restrict__ row_ptr,
                                                  const sk_segment* __restrict__ segs,
-                                                 double* __restrict__ F, uint32_t* __restrict__ perm) {
+                                                 double* __restrict__ F, uint32_t* __restrict__ perm,
+                                                 uint32_t zero_perm) {
   const sk_plan p = plans[plan0 + blockIdx.y];
   if (p.group != G) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
   const long long pair = (long long)blockIdx.x * kF_TPB + threadIdx.x;
   if (pair >= (long long)nA * nB) return;
-  fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm);
+  fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm, zero_perm);
+}
+
+// The inner KM's answer on an all-zero g x g block, replayed once on the host
+// with the same code the device runs (a constant of the algorithm).
+template <int G>
+uint32_t zero_block_perm() {
+  double z[G][G];
+  for (int k = 0; k < G; ++k)
+    for (int l = 0; l < G; ++l) z[k][l] = 0.0;
+  int pm[G];
+  hungarian_small<G>(z, pm);
+  uint32_t packed = 0;
+  for (int k = 0; k < G; ++k) packed |= (uint32_t)pm[k] << (4 * k);
+  return packed;
 }
 
 template <int G>
 int launch_fuse(const sk_plan* d_plans, int p0, int np, long long max_pairs, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
+  static const uint32_t zp = zero_block_perm<G>();
   const long long bx = (max_pairs + kF_TPB - 1) / kF_TPB;
   dim3 grid((unsigned)bx, np);
-  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm);
+  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
   return cuda_check("k_fuse launch");
 }
 
 // ---------------------------------------------------------------------------
-// K2b: outer KM, one warp per plan.  Column j is owned by lane j % 32 and its
-// slack (minv), potential v and used flag live in that lane's registers;
-// row potentials u, match and way live in shared memory.
+// K2b: outer KM, one warp per plan.
+//
+// Column j (0..n) is owned by lane j % 32, slot k = j / 32.  The owner keeps
+// the column's slack minv[j], potential v[j], predecessor way[j] and used bit
+// in registers.  Row potentials are kept per COLUMN (ucol[j] = u[match[j]],
+// shared memory): the reference only ever reads u[i0] with i0 = match[j0]
+// and adds delta to u[match[j]] for used j, so indexing by column removes the
+// match[] indirection from the step's critical path; the augmenting walk
+// moves ucol together with match.  The current row's u starts at 0.0 (it is
+// untouched before its own iteration) and lives in ucol[0].
+//
+// Per Dijkstra step: one predicated cost-row gather, the slack update, a
+// per-lane first-minimum, and a warp argmin that reproduces the reference's
+// "lowest j among equal minima" (mapping.py:103-105) with three redux.sync
+// (order-preserving 64-bit key, -0.0 folded to +0.0 so signed zeros tie as
+// they do under '<'), then delta = the winner's own minv (bit-exact).
 
 constexpr int kO_WARPS = 4;
 
 __host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows) {
   return max_n + 1 > max_rows ? max_n + 1 : max_rows;
 }
-__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows) {
+// Dictionary coding of the fused matrix: real fused weights take few distinct
+// values (2-5 distinct per row), so the warp packs its plan's
+// nA x nB matrix into one-byte codes + a 256-entry table in shared memory and
+// every Dijkstra step gathers its cost row from shared memory instead of L2.
+// A plan with more than 256 distinct values falls back to the L2 gather.
+constexpr int kDictSlots = 256;
+constexpr unsigned long long kEmpty = ~0ull;  // a NaN pattern: never a weight
+
+__host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int max_rows) {
   size_t bytes = (size_t)outer_dbl_elems(max_n, max_rows) * 8 + (size_t)(max_n + 1) * 4 * 2;
   return (bytes + 15) & ~(size_t)15;
+}
+__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, bool coded) {
+  size_t bytes = outer_base_bytes(max_n, max_rows);
+  if (coded) bytes += (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + 15) & ~(size_t)15);
+  return bytes;
 }
 
 struct OuterArgs {
@@ -344,121 +410,179 @@ struct OuterArgs {
   const uint32_t* perm;
   int32_t* assign;
   double* total;
-  int64_t* steps;  // optional: Dijkstra steps per plan (profiling)
+  int64_t* steps;  // optional: {Dijkstra steps, cost loads} per plan (profiling)
   size_t smem_per_warp;
   int max_n;
   int dbl_elems;
 };
 
-template <int CPL>
+__device__ __forceinline__ unsigned long long order_key(double x) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <int CPL, bool CODED>
 __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = blockIdx.x * kO_WARPS + warp;
+  const int q = blockIdx.x * (blockDim.x >> 5) + warp;
   if (q >= A.n_plans) return;
   const sk_plan p = A.plans[q];
-  const int32_t* __restrict__ row_ptr = A.row_ptr;
-  const sk_segment* __restrict__ segs = A.segs;
-  const uint32_t* __restrict__ perm = A.perm;
-  const int max_n = A.max_n;
   const int g = p.group;
   const bool dense = (p.flags & SK_PLAN_DENSE) != 0;
   const int C = p.D * p.P * p.M;
   const int nA = p.rows / g, nB = C / g;
   const int n = nA > nB ? nA : nB;
+  const int n1 = A.max_n + 1;
 
-  // per-warp layout: [double u/wv: dbl_elems] [int match: max_n+1] [int way: max_n+1]
+  // per-warp layout: [double ucol / wv: dbl_elems] [int match: n1] [int way: n1]
   unsigned char* base = smem + (size_t)warp * A.smem_per_warp;
-  const int n1 = max_n + 1;
-  double* u = reinterpret_cast<double*>(base);
+  double* ucol = reinterpret_cast<double*>(base);
   int* match = reinterpret_cast<int*>(base + (size_t)A.dbl_elems * 8);
   int* way = match + n1;
 
-  double v[CPL], minv[CPL];
+  const double* Fp = A.F + p.f_off;
+  // dictionary-code the fused matrix into shared memory (CODED variant)
+  bool coded = false;
+  unsigned long long* table = nullptr;
+  unsigned char* codes = nullptr;
+  if (CODED) {
+    table = reinterpret_cast<unsigned long long*>(base + outer_base_bytes(A.max_n, A.dbl_elems));
+    codes = reinterpret_cast<unsigned char*>(table + kDictSlots);
+    for (int t = lane; t < kDictSlots; t += 32) table[t] = kEmpty;
+    __syncwarp();
+    bool fail = false;
+    const int cnt = nA * nB;
+    for (int e = lane; e < cnt; e += 32) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(__ldg(Fp + e));
+      unsigned h = (unsigned)((bits * 0x9E3779B97F4A7C15ull) >> 56);
+      int tries = 0;
+      while (true) {
+        const unsigned long long old = atomicCAS(table + h, kEmpty, bits);
+        if (old == kEmpty || old == bits) break;
+        h = (h + 1) & (kDictSlots - 1);
+        if (++tries == kDictSlots) {
+          fail = true;
+          break;
+        }
+      }
+      codes[e] = (unsigned char)h;
+    }
+    coded = !__any_sync(kFull, fail);
+    __syncwarp();
+  }
+
+  // static column masks: valid = 1..n, real = 1..nB (beyond: zero padding)
+  unsigned long long valid = 0ull, real = 0ull;
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) v[k] = 0.0;
+  for (int k = 0; k < CPL; ++k) {
+    const int j = lane + 32 * k;
+    if (j >= 1 && j <= n) valid |= 1ull << k;
+    if (j >= 1 && j <= nB) real |= 1ull << k;
+  }
+  double v[CPL], minv[CPL];
+  int wr[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    v[k] = 0.0;
+    wr[k] = 0;
+  }
   for (int j = lane; j <= n; j += 32) {
-    u[j] = 0.0;
+    ucol[j] = 0.0;
     match[j] = 0;
-    way[j] = 0;
   }
   __syncwarp();
 
-  const double* Fp = A.F + p.f_off;
   long long nsteps = 0, nloads = 0;
   for (int i = 1; i <= n; ++i) {
-    if (lane == 0) match[0] = i;
-    unsigned long long used = 0ull;
+    if (lane == 0) {
+      match[0] = i;
+      ucol[0] = 0.0;
+    }
+    unsigned long long used = (lane == 0) ? 1ull : 0ull;  // column 0
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
     __syncwarp();
     int j0 = 0;
     while (true) {
       ++nsteps;
-      if ((j0 & 31) == lane) used |= 1ull << (j0 >> 5);
       const int i0 = match[j0];
-      const double ui0 = u[i0];
-      const bool row_real = (i0 - 1) < nA;
-      const double* rowp = Fp + (long long)(i0 - 1) * nB;
-      // gather this step's cost row (independent loads, MLP = CPL)
+      const double ui0 = ucol[j0];
+      const unsigned long long act = valid & ~used;
+      const unsigned long long ld = (i0 - 1) < nA ? (act & real) : 0ull;
+      const long long rowo = (long long)(i0 - 1) * nB - 1;
       double cst[CPL];
+      if (CODED && coded) {
+        const unsigned char* rowc = codes + rowo;
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        const int j = lane + 32 * k;
-        double x = 0.0;
-        if (row_real && j >= 1 && j <= nB && !((used >> k) & 1ull)) {
-          x = __ldg(rowp + (j - 1));
-          ++nloads;
+        for (int k = 0; k < CPL; ++k) {
+          double x = 0.0;
+          if ((ld >> k) & 1ull) x = __longlong_as_double((long long)table[rowc[lane + 32 * k]]);
+          cst[k] = -x;
         }
-        cst[k] = -x;
+      } else {
+        const double* rowp = Fp + rowo;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          double x = 0.0;
+          if ((ld >> k) & 1ull) x = __ldg(rowp + lane + 32 * k);
+          cst[k] = -x;
+        }
       }
+      nloads += __popcll(ld);
       double best = kInf;
-      int bj = 0x7fffffff;
+      int bk = 0;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        const int j = lane + 32 * k;
-        if (j >= 1 && j <= n && !((used >> k) & 1ull)) {
+        if ((act >> k) & 1ull) {
           const double cur = (cst[k] - ui0) - v[k];
           if (cur < minv[k]) {
             minv[k] = cur;
-            way[j] = j0;
+            wr[k] = j0;
           }
           if (minv[k] < best) {
             best = minv[k];
-            bj = j;
+            bk = k;
           }
         }
       }
+      const unsigned bj = (best < kInf) ? (unsigned)(lane + 32 * bk) : 0xffffffffu;
+      const unsigned long long key = order_key(best);
+      const unsigned hi = __reduce_min_sync(kFull, (unsigned)(key >> 32));
+      const bool c1 = (unsigned)(key >> 32) == hi;
+      const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
+      const bool c2 = c1 && (unsigned)key == lo;
+      const int j1 = (int)__reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
+      const double delta = __shfl_sync(kFull, best, j1 & 31);
+      // a zero delta leaves every potential and slack numerically unchanged
+      // (at most flips the sign of a zero, which no comparison or later
+      // non-zero result can observe), so the update is skipped
+      if (delta != 0.0) {
 #pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double ob = __shfl_xor_sync(kFull, best, off);
-        const int oj = __shfl_xor_sync(kFull, bj, off);
-        if (ob < best || (ob == best && oj < bj)) {
-          best = ob;
-          bj = oj;
-        }
-      }
-      const double delta = best;
-#pragma unroll
-      for (int k = 0; k < CPL; ++k) {
-        const int j = lane + 32 * k;
-        if (j <= n) {
+        for (int k = 0; k < CPL; ++k) {
           if ((used >> k) & 1ull) {
-            u[match[j]] += delta;
+            double* uc = ucol + lane + 32 * k;
+            *uc += delta;
             v[k] -= delta;
-          } else {
+          } else if ((valid >> k) & 1ull) {
             minv[k] -= delta;
           }
         }
       }
-      __syncwarp();
-      j0 = bj;
+      j0 = j1;
+      if ((j0 & 31) == lane) used |= 1ull << (j0 >> 5);
       if (match[j0] == 0) break;
     }
+    // publish predecessors, then walk the augmenting path (lane 0)
+#pragma unroll
+    for (int k = 0; k < CPL; ++k)
+      if (((used | valid) >> k) & 1ull) way[lane + 32 * k] = wr[k];
+    __syncwarp();
     if (lane == 0) {
       while (j0) {
         const int j1 = way[j0];
         match[j0] = match[j1];
+        ucol[j0] = ucol[j1];
         j0 = j1;
       }
     }
@@ -471,14 +595,16 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
     if (r >= 1 && r <= nA) way[r - 1] = j - 1;
   }
   __syncwarp();
-  double* wv = u;
+  double* wv = ucol;
   int32_t* out = A.assign + p.out_off;
+  const int32_t* __restrict__ row_ptr = A.row_ptr;
+  const sk_segment* __restrict__ segs = A.segs;
   for (int r = lane; r < p.rows; r += 32) {
     const int a = r / g, k = r % g;
     const int b = way[a];
     if (b < nB) {
       int col = b * g;
-      if (g > 1) col += (int)((perm[p.f_off + (long long)a * nB + b] >> (4 * k)) & 15u);
+      if (g > 1) col += (int)((A.perm[p.f_off + (long long)a * nB + b] >> (4 * k)) & 15u);
       const double w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
       out[r] = col;
       wv[r] = w;
@@ -491,16 +617,19 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   if (A.steps) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);
-    if (lane == 0) A.steps[2 * q + 1] = nloads;
+    if (lane == 0) {
+      A.steps[2 * q] = nsteps;
+      A.steps[2 * q + 1] = nloads;
+    }
   }
   if (lane == 0) {
+    // total_weight in the reference's order (mapping.py:143-148 / 274-282)
     double t = 0.0;
     for (int r = 0; r < p.rows; ++r) {
       const double w = wv[r];
       if (w >= 0.0) t += w;
     }
     A.total[q] = t;
-    if (A.steps) A.steps[2 * q] = nsteps;
   }
 }
 
@@ -596,29 +725,55 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
 
 template <int CPL>
 int launch_outer(OuterArgs A, int max_rows, cudaStream_t s) {
-  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows);
   A.dbl_elems = outer_dbl_elems(A.max_n, max_rows);
-  const size_t smem = A.smem_per_warp * kO_WARPS;
+  constexpr size_t kSmemCap = 200 * 1024;
+  // coded variant when a block of >= 2 warps fits; fewer warps per block for
+  // big plans so the codes still fit
+  const size_t coded_warp = outer_smem_per_warp(A.max_n, max_rows, true);
+  int warps = kO_WARPS;
+  bool coded = true;
+  while (warps > 1 && coded_warp * warps > kSmemCap) --warps;
+  if (coded_warp * warps > kSmemCap) {
+    coded = false;
+    warps = kO_WARPS;
+  }
+  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows, coded);
+  const size_t smem = A.smem_per_warp * warps;
   if (smem > 227 * 1024) return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", smem);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_outer<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_outer<CPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_outer<CPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  const int blocks = (A.n_plans + kO_WARPS - 1) / kO_WARPS;
-  k_outer<CPL><<<blocks, kO_WARPS * 32, smem, s>>>(A);
+  const int blocks = (A.n_plans + warps - 1) / warps;
+  if (coded)
+    k_outer<CPL, true><<<blocks, warps * 32, smem, s>>>(A);
+  else
+    k_outer<CPL, false><<<blocks, warps * 32, smem, s>>>(A);
   return cuda_check("k_outer launch");
 }
 
 int outer_dispatch(const OuterArgs& A, int max_rows, cudaStream_t s) {
-  const int need = A.max_n + 1;
-  if (need <= 32) return launch_outer<1>(A, max_rows, s);
-  if (need <= 64) return launch_outer<2>(A, max_rows, s);
-  if (need <= 128) return launch_outer<4>(A, max_rows, s);
-  if (need <= 256) return launch_outer<8>(A, max_rows, s);
-  if (need <= 512) return launch_outer<16>(A, max_rows, s);
-  if (need <= 32 * 33) return launch_outer<33>(A, max_rows, s);
-  if (need <= 32 * 64) return launch_outer<64>(A, max_rows, s);
+  const int need = (A.max_n + 1 + 31) / 32;  // columns per lane
+  switch (need) {
+    case 0:
+    case 1: return launch_outer<1>(A, max_rows, s);
+    case 2: return launch_outer<2>(A, max_rows, s);
+    case 3: return launch_outer<3>(A, max_rows, s);
+    case 4: return launch_outer<4>(A, max_rows, s);
+    case 5: return launch_outer<5>(A, max_rows, s);
+    case 6: return launch_outer<6>(A, max_rows, s);
+    case 7:
+    case 8: return launch_outer<8>(A, max_rows, s);
+    default: break;
+  }
+  if (need <= 12) return launch_outer<12>(A, max_rows, s);
+  if (need <= 17) return launch_outer<17>(A, max_rows, s);
+  if (need <= 24) return launch_outer<24>(A, max_rows, s);
+  if (need <= 33) return launch_outer<33>(A, max_rows, s);
+  if (need <= 48) return launch_outer<48>(A, max_rows, s);
+  if (need <= 64) return launch_outer<64>(A, max_rows, s);
   return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", A.max_n);
 }
 

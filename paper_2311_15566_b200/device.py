@@ -44,19 +44,25 @@ class MapBatch:
         return len(self.plans) - 1
 
     # -- layout ---------------------------------------------------------------
-    def _layout(self, dense_cols: bool):
+    def _layout(self, dense_cols: bool, order=None):
+        """Plans in `order` (default: insertion order); returns arrays in that
+        order plus summary sizes."""
         Q = len(self.plans)
+        order = list(range(Q)) if order is None else list(order)
         plans = np.zeros(Q, dtype=nat.PLAN)
         seg_base = row_base = f_off = out_off = 0
         rp_parts = []
         max_pairs = max_n = max_rows = max_cols = 0
         gmask = 0
-        for q, (R, D, P, M, L, K, g, flags) in enumerate(self.plans):
+        seg_parts = []
+        for slot, q in enumerate(order):
+            R, D, P, M, L, K, g, flags = self.plans[q]
             C = D * P * M
             nA, nB = R // g, C // g
             pairs = R * C if dense_cols else nA * nB
-            plans[q] = (R, D, P, M, L, K, g, flags, row_base, 0, f_off, out_off, 0)
+            plans[slot] = (R, D, P, M, L, K, g, flags, row_base, 0, f_off, out_off, 0)
             rp_parts.append(self.row_ptrs[q][:-1].astype(np.int64) + seg_base)
+            seg_parts.append(self.segs[q])
             seg_base += len(self.segs[q])
             row_base += R
             f_off += pairs
@@ -68,7 +74,7 @@ class MapBatch:
             gmask |= 1 << g
         rp_parts.append(np.array([seg_base], dtype=np.int64))
         row_ptr = np.concatenate(rp_parts).astype(np.int32)
-        segs = np.concatenate(self.segs) if self.segs else np.zeros(0, dtype=nat.SEGMENT)
+        segs = np.concatenate(seg_parts) if seg_parts else np.zeros(0, dtype=nat.SEGMENT)
         info = dict(Q=Q, rows=row_base, pairs=f_off, max_pairs=max_pairs, max_n=max_n,
                     max_rows=max_rows, max_cols=max_cols, gmask=gmask)
         return plans, row_ptr, segs, info
@@ -90,9 +96,16 @@ class MapBatch:
 
     # -- K2: map_devices ----------------------------------------------------------
     def run_map(self, mapping_error=ValueError):
-        """-> (assign int32 [sum R] (col or -1), totals float64 [Q], out_off per plan)."""
+        """-> (assign int32 [sum R] (col or -1), totals float64 [Q], out_off per plan),
+        all indexed by insertion order."""
+        from .sweep import outer_classes
+
         lib = nat.load()
-        plans, row_ptr, segs, info = self._layout(dense_cols=False)
+        n_of = []
+        for (R, D, P, M, L, K, g, flags) in self.plans:
+            n_of.append(max(R // g, (D * P * M) // g))
+        order = sorted(range(len(self.plans)), key=lambda q: (-n_of[q], q))
+        plans, row_ptr, segs, info = self._layout(dense_cols=False, order=order)
         dev_in, (p_plans, p_rp, p_segs) = self._upload(plans, row_ptr, segs)
         dev = _device()
         Q, rows = info["Q"], info["rows"]
@@ -101,15 +114,26 @@ class MapBatch:
         out = torch.empty(_align(8 * Q + 4 * rows) // 8 + 1, dtype=torch.float64, device=dev)
         p_total = out.data_ptr()
         p_assign = p_total + 8 * Q
-        rc = lib.sk_map_batched(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
-                                p_assign, p_total, info["max_pairs"], info["max_n"],
-                                info["max_rows"], info["gmask"], _stream_ptr())
+        st = _stream_ptr()
+        rc = lib.sk_map_fuse(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
+                             info["max_pairs"], info["gmask"], st)
         nat.check(rc, mapping_error)
+        ns = np.array([n_of[q] for q in order], dtype=np.int64)
+        for a, b, mn in outer_classes(ns):
+            mr = int(plans["rows"][a:b].max())
+            rc = lib.sk_map_outer(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                  perm.data_ptr(), p_assign, p_total + 8 * a, 0, mn, mr, st)
+            nat.check(rc, mapping_error)
         host = out.cpu().numpy().view(np.uint8)
         del dev_in
-        totals = host[:8 * Q].view(np.float64).copy()
+        totals_sorted = host[:8 * Q].view(np.float64)
         assign = host[8 * Q:8 * Q + 4 * rows].view(np.int32).copy()
-        return assign, totals, plans["out_off"].astype(np.int64)
+        totals = np.empty(Q, dtype=np.float64)
+        out_off = np.empty(Q, dtype=np.int64)
+        for slot, q in enumerate(order):
+            totals[q] = totals_sorted[slot]
+            out_off[q] = plans["out_off"][slot]
+        return assign, totals, out_off
 
     # -- K1: build_graph -----------------------------------------------------------
     def run_weights(self, mapping_error=ValueError):

@@ -112,6 +112,14 @@ def make_sweep(n_positions: int, sets_per_pair: int, seed: int = 0, G: int = 4, 
         tok_off += S * oD
     desc = np.concatenate(descs)
     plan = np.concatenate(plans)
+    # largest outer problems first: contiguous size classes for the outer-KM
+    # launches and longest-first scheduling inside each launch
+    R = plan["rows"].astype(np.int64)
+    g = plan["group"].astype(np.int64)
+    C = (plan["D"] * plan["P"] * plan["M"]).astype(np.int64)
+    n_outer = np.maximum(R // g, C // g)
+    order = np.lexsort((np.arange(len(plan)), -(n_outer * (C // g)), -n_outer))
+    desc, plan = desc[order], plan[order]
     desc["plan"] = np.arange(len(plan))
     R = plan["rows"].astype(np.int64)
     g = plan["group"].astype(np.int64)
@@ -130,6 +138,35 @@ def _align(n: int, a: int = 256) -> int:
     return (n + a - 1) // a * a
 
 
+_CPL_BUCKETS = (1, 2, 3, 4, 5, 6, 8, 8, 12, 12, 12, 12, 17, 17, 17, 17, 17, 24, 24, 24, 24, 24, 24,
+                24, 33, 33, 33, 33, 33, 33, 33, 33, 33)
+
+
+def cpl_bucket(n: int) -> int:
+    """Columns-per-lane template the outer-KM dispatch picks for size n
+    (mirrors outer_dispatch in spotkm.cu)."""
+    need = max(1, (n + 1 + 31) // 32)
+    if need <= len(_CPL_BUCKETS):
+        return _CPL_BUCKETS[need - 1]
+    return 48 if need <= 48 else 64
+
+
+def outer_classes(n_outer: np.ndarray):
+    """Contiguous (start, stop, max_n) ranges of plans sharing one outer-KM
+    template; plans must be sorted by n descending."""
+    out = []
+    start = 0
+    N = len(n_outer)
+    while start < N:
+        b = cpl_bucket(int(n_outer[start]))
+        stop = start + 1
+        while stop < N and cpl_bucket(int(n_outer[stop])) == b:
+            stop += 1
+        out.append((start, stop, int(n_outer[start:stop].max())))
+        start = stop
+    return out
+
+
 class SweepRunner:
     """Device buffers for one SweepBatch; `run()` = one pass of the hot path.
 
@@ -145,6 +182,8 @@ class SweepRunner:
         st = batch.stats()
         self.max_pairs = int(st["pairs"].max())
         self.max_n = int(st["n"].max())
+        self.classes = outer_classes(st["n"])
+        self.class_rows = [int(st["rows"][a:b].max()) for a, b, _ in self.classes]
         self.max_rows = int(st["rows"].max())
         self.gmask = int(np.bitwise_or.reduce(1 << batch.plans["group"].astype(np.int64)))
         parts = [batch.desc, batch.plans, batch.alive, batch.tok]
@@ -200,11 +239,13 @@ class SweepRunner:
         if marks:
             marks[2].record()
         out = self.d_out.data_ptr()
-        rc = self.lib.sk_map_outer(p_plans, Q, self.row_ptr.data_ptr(), self.segs.data_ptr(),
-                                   self.fused.data_ptr(), self.perm.data_ptr(), out + 8 * Q, out,
-                                   0 if steps is None else steps.data_ptr(), self.max_n,
-                                   self.max_rows, st)
-        nat.check(rc)
+        for (a, b, mn), mr in zip(self.classes, self.class_rows):
+            rc = self.lib.sk_map_outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
+                                       self.segs.data_ptr(), self.fused.data_ptr(),
+                                       self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
+                                       0 if steps is None else steps.data_ptr() + 16 * a, mn, mr,
+                                       st)
+            nat.check(rc)
         if marks:
             marks[3].record()
 
