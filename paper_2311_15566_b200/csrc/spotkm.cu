@@ -453,20 +453,36 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
     __syncwarp();
     bool fail = false;
     const int cnt = nA * nB;
-    for (int e = lane; e < cnt; e += 32) {
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(__ldg(Fp + e));
-      unsigned h = (unsigned)((bits * 0x9E3779B97F4A7C15ull) >> 56);
-      int tries = 0;
-      while (true) {
-        const unsigned long long old = atomicCAS(table + h, kEmpty, bits);
-        if (old == kEmpty || old == bits) break;
-        h = (h + 1) & (kDictSlots - 1);
-        if (++tries == kDictSlots) {
-          fail = true;
-          break;
-        }
+    constexpr int U = 8;  // independent loads in flight per lane
+    for (int e0 = 0; e0 < cnt; e0 += 32 * U) {
+      unsigned long long bits[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 32 + lane;
+        bits[u] = e < cnt ? (unsigned long long)__double_as_longlong(__ldg(Fp + e)) : kEmpty;
       }
-      codes[e] = (unsigned char)h;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * 32 + lane;
+        // one insert per distinct value per warp: the lowest lane holding it
+        const unsigned peers = __match_any_sync(kFull, bits[u]);
+        const int leader = __ffs(peers) - 1;
+        unsigned h = 0;
+        if (lane == leader && bits[u] != kEmpty) {
+          h = (unsigned)((bits[u] * 0x9E3779B97F4A7C15ull) >> 56);
+          for (int tries = 0;; ++tries) {
+            const unsigned long long old = atomicCAS(table + h, kEmpty, bits[u]);
+            if (old == kEmpty || old == bits[u]) break;
+            h = (h + 1) & (kDictSlots - 1);
+            if (tries + 1 == kDictSlots) {
+              fail = true;
+              break;
+            }
+          }
+        }
+        h = __shfl_sync(kFull, h, leader);
+        if (e < cnt) codes[e] = (unsigned char)h;
+      }
     }
     coded = !__any_sync(kFull, fail);
     __syncwarp();
@@ -534,17 +550,15 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       int bk = 0;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        if ((act >> k) & 1ull) {
-          const double cur = (cst[k] - ui0) - v[k];
-          if (cur < minv[k]) {
-            minv[k] = cur;
-            wr[k] = j0;
-          }
-          if (minv[k] < best) {
-            best = minv[k];
-            bk = k;
-          }
-        }
+        const bool on = (act >> k) & 1ull;
+        const double cur = (cst[k] - ui0) - v[k];
+        const bool imp = on && cur < minv[k];
+        minv[k] = imp ? cur : minv[k];
+        wr[k] = imp ? j0 : wr[k];
+        const double mk = on ? minv[k] : kInf;
+        const bool better = mk < best;
+        best = better ? mk : best;
+        bk = better ? k : bk;
       }
       const unsigned bj = (best < kInf) ? (unsigned)(lane + 32 * bk) : 0xffffffffu;
       const unsigned long long key = order_key(best);
@@ -560,13 +574,10 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       if (delta != 0.0) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          if ((used >> k) & 1ull) {
-            double* uc = ucol + lane + 32 * k;
-            *uc += delta;
-            v[k] -= delta;
-          } else if ((valid >> k) & 1ull) {
-            minv[k] -= delta;
-          }
+          const bool u = (used >> k) & 1ull;
+          if (u) ucol[lane + 32 * k] += delta;
+          v[k] = u ? v[k] - delta : v[k];
+          minv[k] = (!u && ((valid >> k) & 1ull)) ? minv[k] - delta : minv[k];
         }
       }
       j0 = j1;

@@ -209,6 +209,8 @@ class SweepRunner:
         self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8, pin_memory=True)
         self.d2h_bytes = 8 * Q + 4 * R
         self.stream = stream
+        # one side stream per outer-KM size class so the classes' tails overlap
+        self.side = [torch.cuda.Stream(self.dev) for _ in self.classes]
 
     def _s(self) -> int:
         return (self.stream or torch.cuda.current_stream(self.dev)).cuda_stream
@@ -239,13 +241,20 @@ class SweepRunner:
         if marks:
             marks[2].record()
         out = self.d_out.data_ptr()
-        for (a, b, mn), mr in zip(self.classes, self.class_rows):
+        main = self.stream or torch.cuda.current_stream(self.dev)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for ((a, b, mn), mr), side in zip(zip(self.classes, self.class_rows), self.side):
+            side.wait_event(fork)
             rc = self.lib.sk_map_outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
                                        self.segs.data_ptr(), self.fused.data_ptr(),
                                        self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
                                        0 if steps is None else steps.data_ptr() + 16 * a, mn, mr,
-                                       st)
+                                       side.cuda_stream)
             nat.check(rc)
+            done = torch.cuda.Event()
+            done.record(side)
+            main.wait_event(done)
         if marks:
             marks[3].record()
 
