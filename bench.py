@@ -263,6 +263,7 @@ def run_reference(args):
 
 
 def measure_ours(runner, K, W, world, rank, local, flush, count_launches):
+    """-> (device ms over K steps, e2e ms over K steps, clocks, launches)."""
     import torch
 
     for _ in range(W):
@@ -272,18 +273,18 @@ def measure_ours(runner, K, W, world, rank, local, flush, count_launches):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    phase = np.zeros(3)
     dev_ms = 0.0
     launches = 0
     for k in range(K):
         flush.fill_(k & 0xff)                       # evict L2 outside the timed window
-        marks = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        runner.solve(marks=marks)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        runner.solve()
+        e1.record()
         launches += count_launches
-        torch.cuda.synchronize()
-        ph = [marks[i].elapsed_time(marks[i + 1]) for i in range(3)]
-        phase += ph
-        dev_ms += marks[0].elapsed_time(marks[3])
+        e1.synchronize()
+        dev_ms += e0.elapsed_time(e1)
     torch.cuda.synchronize()
     barrier(world)
     e2e_ms = 0.0
@@ -301,7 +302,25 @@ def measure_ours(runner, K, W, world, rank, local, flush, count_launches):
         e2e_ms += e0.elapsed_time(e1)
     clk = clocks.stop()
     barrier(world)
-    return dev_ms, e2e_ms, phase, clk, launches
+    return dev_ms, e2e_ms, clk, launches
+
+
+def kernel_breakdown(runner, flush, reps=2):
+    """Serialised, event-bracketed launches (untimed for `value`): per-kernel
+    ms per step plus the outer KM's Dijkstra-step / cost-load counters."""
+    import torch
+
+    Q = runner.b.n_plans
+    acc: dict[str, float] = {}
+    steps = torch.zeros(2 * Q, dtype=torch.int64, device="cuda")
+    for r in range(reps):
+        flush.fill_(r & 0xff)
+        prof = {}
+        runner.solve(steps=steps, profile=prof)
+        torch.cuda.synchronize()
+        for k, v in runner.kernel_ms(prof).items():
+            acc[k] = acc.get(k, 0.0) + v / reps
+    return acc, steps.cpu().numpy().reshape(-1, 2)
 
 
 def run_ours(args):
@@ -313,30 +332,31 @@ def run_ours(args):
     geom, shapes = sweep.MODELS[args.model]
     batch = sweep.make_sweep(args.positions, args.sets, seed=1000 + rank, model=geom, shapes=shapes)
     runner = sweep.SweepRunner(batch)
-    n_groups = bin(runner.gmask).count("1")
-    per_step_launches = 1 + n_groups + len(runner.classes)
+    per_step_launches = 1 + sum(bin(m).count("1") for m in runner.class_gmask) + len(runner.classes)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     K, W = args.steps, args.warmup
-    dev_ms, e2e_ms, phase, clk, launches = measure_ours(runner, K, W, world, rank, local, flush,
-                                                        per_step_launches)
+    dev_ms, e2e_ms, clk, launches = measure_ours(runner, K, W, world, rank, local, flush,
+                                                 per_step_launches)
     dev_ms_max = allreduce_max(dev_ms, world)
     e2e_ms_max = allreduce_max(e2e_ms, world)
     plans_all = allreduce_sum(float(batch.n_plans * K), world)
     value = plans_all / (dev_ms_max / 1e3)
     e2e_value = plans_all / (e2e_ms_max / 1e3)
 
-    # algorithmic work of the outer KM (one extra, untimed pass with counters)
-    steps = torch.zeros(2 * batch.n_plans, dtype=torch.int64, device="cuda")
-    runner.solve(steps=steps)
-    torch.cuda.synchronize()
-    st = steps.cpu().numpy().reshape(-1, 2)
+    kms, st = kernel_breakdown(runner, flush)
     stats = batch.stats()
+    nA, nB = stats["nA"], stats["nB"]
+    # algorithmic HBM bytes per launch-set (per step):
+    #   k_sweep_expand: writes 2 segments (64 B) + row_ptr (4 B) per row, reads descriptors
+    #   k_fuse: reads 2 segments per row once + writes fused weight (8 B) + perm (4 B) per pair
+    #   k_outer: reads the fused matrix once (8 B per pair), writes assign + total
     kernels = {
-        "k_sweep_expand": {"ms": phase[0] / K, "bytes": int(64 * batch.rows + 48 * batch.n_plans)},
-        "k_fuse": {"ms": phase[1] / K,
+        "k_sweep_expand": {"ms": kms.get("k_sweep_expand", 0.0),
+                           "bytes": int(68 * batch.rows + 112 * batch.n_plans)},
+        "k_fuse": {"ms": kms.get("k_fuse", 0.0),
                    "bytes": int(12 * stats["pairs"].sum() + 64 * batch.rows)},
-        "k_outer": {"ms": phase[2] / K,
-                    "bytes": int(8 * st[:, 1].sum() + 4 * batch.rows + 8 * batch.n_plans)},
+        "k_outer": {"ms": kms.get("k_outer", 0.0),
+                    "bytes": int(8 * stats["pairs"].sum() + 4 * batch.rows + 8 * batch.n_plans)},
     }
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     pk, src = peaks()
@@ -347,8 +367,8 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": traffic, "peak_source": src,
                 "algorithmic_bytes_per_launch": kernels[dom]["bytes"],
-                "note": "k_outer bytes = cost-row element loads x 8 B counted on device "
-                        "(Dijkstra steps are sequential per plan: latency-bound)"}
+                "note": "per step, all size classes of the kernel; the outer KM is a sequential "
+                        "Dijkstra chain per plan (latency-bound), see outer_km"}
     survey_bytes = 16.0 * float((stats["rows"] * stats["cols"]).sum()) / batch.n_plans
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -361,9 +381,10 @@ def run_ours(args):
                    "l2": "flushed between timed steps (512 MiB device write, outside the events)",
                    "parallelism": f"plan-sharded x{world} (no collective)"},
         "roofline": roofline,
-        "kernels_ms_per_step": {k: v["ms"] for k, v in kernels.items()},
+        "kernels_ms_per_step_serialized": {k: v["ms"] for k, v in kernels.items()},
         "outer_km": {"dijkstra_steps_per_plan": float(st[:, 0].mean()),
-                     "steps_per_s": float(st[:, 0].sum()) / (kernels["k_outer"]["ms"] / 1e3)},
+                     "steps_per_s": float(st[:, 0].sum()) / (kernels["k_outer"]["ms"] / 1e3),
+                     "cost_loads_per_plan": float(st[:, 1].mean())},
         "survey_roofline": {"bytes_per_plan_16RC": survey_bytes,
                             "ceiling_plans_per_s": hbm * 1e9 / survey_bytes,
                             "frac": value / world / (hbm * 1e9 / survey_bytes)},
@@ -391,13 +412,13 @@ def run_ours(args):
             sets = {64: 256, 128: 256, 256: 256, 512: 64, 1024: 32}[n_pos]
             b = sweep.make_sweep(n_pos, sets, seed=2000 + rank, model=geom, shapes=shapes)
             r = sweep.SweepRunner(b)
-            d_ms, x_ms, ph, _, _ = measure_ours(r, max(2, K // 2), 2, world, rank, local, flush,
-                                               0)
             k2 = max(2, K // 2)
+            d_ms, x_ms, _, _ = measure_ours(r, k2, 2, world, rank, local, flush, 0)
+            km, _ = kernel_breakdown(r, flush, 1)
             sizes[str(n_pos)] = {"plans_per_step": b.n_plans,
                                  "plans_per_s": b.n_plans * k2 / (d_ms / 1e3),
                                  "e2e_plans_per_s": b.n_plans * k2 / (x_ms / 1e3),
-                                 "kernels_ms": (ph / k2).tolist()}
+                                 "kernels_ms_serialized": km}
             del r
         line["sweep_sizes"] = sizes
     if rank == 0:

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
 // K2a: per fused pair (a, b): g x g block -> inner KM -> fused weight + perm
 
 constexpr int kF_TPB = 128;
+constexpr int kF_PPT = 1;  // fused pairs per thread
 
 template <int G>
 __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB,
@@ -331,9 +332,14 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   if (p.group != G) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
-  const long long pair = (long long)blockIdx.x * kF_TPB + threadIdx.x;
-  if (pair >= (long long)nA * nB) return;
-  fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm, zero_perm);
+  const long long total = (long long)nA * nB;
+  const long long base = (long long)blockIdx.x * (kF_TPB * kF_PPT) + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < kF_PPT; ++i) {
+    const long long pair = base + (long long)i * kF_TPB;
+    if (pair < total)
+      fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm, zero_perm);
+  }
 }
 
 // The inner KM's answer on an all-zero g x g block, replayed once on the host
@@ -354,7 +360,7 @@ template <int G>
 int launch_fuse(const sk_plan* d_plans, int p0, int np, long long max_pairs, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
   static const uint32_t zp = zero_block_perm<G>();
-  const long long bx = (max_pairs + kF_TPB - 1) / kF_TPB;
+  const long long bx = (max_pairs + kF_TPB * kF_PPT - 1) / (kF_TPB * kF_PPT);
   dim3 grid((unsigned)bx, np);
   k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
   return cuda_check("k_fuse launch");

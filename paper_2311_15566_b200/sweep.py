@@ -184,6 +184,9 @@ class SweepRunner:
         self.max_n = int(st["n"].max())
         self.classes = outer_classes(st["n"])
         self.class_rows = [int(st["rows"][a:b].max()) for a, b, _ in self.classes]
+        self.class_pairs = [int(st["pairs"][a:b].max()) for a, b, _ in self.classes]
+        self.class_gmask = [int(np.bitwise_or.reduce(1 << batch.plans["group"][a:b].astype(np.int64)))
+                            for a, b, _ in self.classes]
         self.max_rows = int(st["rows"].max())
         self.gmask = int(np.bitwise_or.reduce(1 << batch.plans["group"].astype(np.int64)))
         parts = [batch.desc, batch.plans, batch.alive, batch.tok]
@@ -218,45 +221,69 @@ class SweepRunner:
     def upload(self):
         self.d_in.copy_(self.h_in, non_blocking=True)
 
-    def solve(self, marks=None, steps=None):
-        """Expand + fused inner KM + outer KM on the runner's stream.
-        marks: optional list of 4 torch.cuda.Event recorded at the phase
-        boundaries (expand | fuse | outer); steps: optional int64 device tensor
-        [2*Q] receiving {Dijkstra steps, cost loads} per plan."""
+    def solve(self, steps=None, profile=None):
+        """One pass of the hot path on the runner's stream: expand, then per
+        outer-KM size class the fused inner KMs and the outer KM, each class
+        on its own stream so the classes' tails overlap.
+
+        steps: optional int64 device tensor [2*Q] receiving {Dijkstra steps,
+        cost loads} per plan.  profile: optional dict; when given, the launches
+        are serialised on the main stream and bracketed with CUDA events so
+        per-kernel times can be read back (profile["events"])."""
         base = self.d_in.data_ptr()
         p_desc, p_plans, p_alive, p_tok = (base + o for o in self.offs)
         Q = self.b.n_plans
-        st = self._s()
-        if marks:
-            marks[0].record()
-        rc = self.lib.sk_sweep_expand(p_desc, Q, p_alive, p_tok, p_plans, self.row_ptr.data_ptr(),
-                                      self.segs.data_ptr(), self.max_rows, st)
-        nat.check(rc)
-        if marks:
-            marks[1].record()
-        rc = self.lib.sk_map_fuse(p_plans, Q, self.row_ptr.data_ptr(), self.segs.data_ptr(),
-                                  self.fused.data_ptr(), self.perm.data_ptr(), self.max_pairs,
-                                  self.gmask, st)
-        nat.check(rc)
-        if marks:
-            marks[2].record()
-        out = self.d_out.data_ptr()
         main = self.stream or torch.cuda.current_stream(self.dev)
+        evs = []
+
+        def mark(tag):
+            if profile is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(main)
+                evs.append((tag, e))
+
+        mark("start")
+        rc = self.lib.sk_sweep_expand(p_desc, Q, p_alive, p_tok, p_plans, self.row_ptr.data_ptr(),
+                                      self.segs.data_ptr(), self.max_rows, main.cuda_stream)
+        nat.check(rc)
+        mark("k_sweep_expand")
+        out = self.d_out.data_ptr()
         fork = torch.cuda.Event()
         fork.record(main)
-        for ((a, b, mn), mr), side in zip(zip(self.classes, self.class_rows), self.side):
-            side.wait_event(fork)
+        for c, ((a, b, mn), side) in enumerate(zip(self.classes, self.side)):
+            st = side
+            if profile is None:
+                side.wait_event(fork)
+            else:
+                st = main
+            rc = self.lib.sk_map_fuse(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
+                                      self.segs.data_ptr(), self.fused.data_ptr(),
+                                      self.perm.data_ptr(), self.class_pairs[c],
+                                      self.class_gmask[c], st.cuda_stream)
+            nat.check(rc)
+            mark("k_fuse")
             rc = self.lib.sk_map_outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
                                        self.segs.data_ptr(), self.fused.data_ptr(),
                                        self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
-                                       0 if steps is None else steps.data_ptr() + 16 * a, mn, mr,
-                                       side.cuda_stream)
+                                       0 if steps is None else steps.data_ptr() + 16 * a, mn,
+                                       self.class_rows[c], st.cuda_stream)
             nat.check(rc)
-            done = torch.cuda.Event()
-            done.record(side)
-            main.wait_event(done)
-        if marks:
-            marks[3].record()
+            mark("k_outer")
+            if profile is None:
+                done = torch.cuda.Event()
+                done.record(side)
+                main.wait_event(done)
+        if profile is not None:
+            profile["events"] = evs
+
+    @staticmethod
+    def kernel_ms(profile):
+        """Per-kernel milliseconds from a profiled solve (after synchronize)."""
+        evs = profile["events"]
+        out: dict[str, float] = {}
+        for (_, e0), (tag, e1) in zip(evs, evs[1:]):
+            out[tag] = out.get(tag, 0.0) + e0.elapsed_time(e1)
+        return out
 
     def download(self):
         self.h_out.copy_(self.d_out, non_blocking=True)
