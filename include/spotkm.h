@@ -176,6 +176,99 @@ int sk_copy_batched(const sk_copy* d_copies, int n_copies, int n_ctas, void* str
 /* Peer-access helper: enable access from `device` to each of `peers`. */
 int sk_enable_peer_access(int device, const int* peers, int n_peers);
 
+/* ------------------------------------------------------------------------
+ * Migration planner (host, native, bit-exact) -- replaces plan_migration
+ * (migration.py:311-384) incl. derive_transfers (201-305), _cover_from_holders
+ * (149-194), memopt_layer_order (89-143) and simulate_buffer_usage (387-401).
+ * Interval endpoints are integer numerators over K (lcm of every interval
+ * denominator and M); GPUs are given in the reference's sorted order
+ * (natural_key(instance), local index); instances carry their natural-key
+ * rank, plain string rank (release sorting) and departing flag.
+ */
+typedef struct sk_mig_input {
+  int32_t n_inst, n_gpus;
+  const int32_t* inst_natrank;
+  const int32_t* inst_strrank;
+  const uint8_t* inst_departing;
+  const int32_t* gpu_inst;
+  const int32_t* gpu_local;
+  const int32_t* gpu_pos;       /* flat target position ((d-1)*P+(p-1))*M+(m-1), or -1 */
+  const int32_t* model_ptr;     /* [n_gpus+1] */
+  const int64_t* model_shards;  /* (layer, lo, hi) triples, inventory order */
+  const int32_t* cache_ptr;     /* [n_gpus+1] */
+  const int64_t* cache_shards;  /* (rid, layer, lo, hi, tokens), inventory order */
+  int32_t D, P, M, L;
+  int64_t bpl, kv, K;
+  const int32_t* inh_ptr;       /* [D+2] CSR over new pipelines 1..D, or NULL */
+  const int64_t* inh_items;     /* (rid, tokens) pairs in inherited order */
+  int32_t has_umax, reserved;
+  double u_max;
+} sk_mig_input;
+
+typedef struct sk_mig_transfer {
+  int32_t kind, layer; /* kind 0 model, 1 cache */
+  int64_t lo, hi;      /* numerators over K */
+  int32_t src, dst;    /* gpu indices (input order) */
+  double bytes;
+  int64_t rid, tokens; /* rid -1 for model transfers */
+} sk_mig_transfer;
+
+typedef struct sk_mig_action {
+  int32_t kind; /* 0 migrate_cache, 1 migrate_layer, 2 start_stage */
+  int32_t layer, stage;
+  int32_t tr_begin, tr_end, rel_begin, rel_end;
+  int32_t reserved;
+} sk_mig_action;
+
+typedef struct sk_mig_release {
+  int32_t inst, layer;
+  double bytes;
+} sk_mig_release;
+
+typedef struct sk_mig_result sk_mig_result; /* opaque, library-owned */
+
+/* derive_only != 0: stop after derive_transfers; the result then holds the
+ * model transfers (first) and cache transfers, cache releases in `releases`
+ * and per-layer releases in `layer_releases`, all in the reference's order.
+ * SK_ENOSOURCE: sk_planner_error() holds "<lo> <hi>" numerators of the
+ * uncovered piece. */
+int sk_plan_migration(const sk_mig_input* in, int derive_only, sk_mig_result** out);
+/* counts[7] = {transfers, actions, action_transfers, releases, peak entries,
+ *              layer_releases, model transfers} */
+int sk_mig_counts(const sk_mig_result* r, int64_t* counts);
+int sk_mig_export(const sk_mig_result* r, sk_mig_transfer* transfers, sk_mig_action* actions,
+                  int32_t* action_transfers, sk_mig_release* releases, double* peak,
+                  sk_mig_release* layer_releases);
+void sk_mig_free(sk_mig_result* r);
+const char* sk_planner_error(void);
+
+/* plan_timeline (costmodel.py:189-228): per-action completion times under
+ * per-instance full-duplex link serialisation; migration_cost (231-260) is
+ * the caller's scalar reduction of these. */
+typedef struct sk_timeline_input {
+  int32_t n_inst, n_actions;
+  const int32_t* action_ptr; /* [n_actions+1] into the transfer arrays */
+  const int32_t* src_inst;
+  const int32_t* dst_inst;
+  const double* bytes;
+  double bandwidth, latency, start;
+  const uint8_t* has_release; /* per instance, or NULL */
+  const double* release;
+} sk_timeline_input;
+
+int sk_plan_timeline(const sk_timeline_input* t, double* ends);
+
+/* memopt_layer_order (migration.py:114-143) on per-layer traffic given as CSR
+ * lists of (instance, bytes): incoming[l] and freed[l] for l in 0..L-1.
+ * order receives L layer indices. */
+int sk_memopt_order(int32_t n_layers, int32_t n_inst, const int32_t* in_ptr, const int32_t* in_inst,
+                    const double* in_bytes, const int32_t* fr_ptr, const int32_t* fr_inst,
+                    const double* fr_bytes, int32_t has_umax, double u_max, int32_t* order);
+
+/* Correctly rounded (num_hi * 2^64 + num_lo) / den as a double, num >= 0,
+ * den > 0: the conversion float(Fraction) performs (utility, exposed for tests). */
+double sk_rat_to_double(int64_t num_hi, uint64_t num_lo, int64_t den);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,3 +30,14 @@ from .mapping import (  # noqa: F401
     map_devices_many,
 )
 from .migration import MigrationAction, MigrationError, MigrationPlan, Transfer  # noqa: F401
+from .planner import (  # noqa: F401
+    LayerTraffic,
+    derive_transfers,
+    memopt_layer_order,
+    migration_cost,
+    plan_from_dict,
+    plan_migration,
+    plan_timeline,
+    plan_to_dict,
+    simulate_buffer_usage,
+)

@@ -38,6 +38,8 @@ EXPORTS = (
     "sk_abi_version", "sk_last_error", "sk_build_weights", "sk_map_batched", "sk_map_fuse",
     "sk_map_outer", "sk_km_dense",
     "sk_sweep_expand", "sk_copy_batched", "sk_enable_peer_access",
+    "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
+    "sk_plan_timeline", "sk_memopt_order",
 )
 
 

@@ -15,7 +15,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = [PKG / "csrc" / "spotkm.cu"]
+SRC = [PKG / "csrc" / "spotkm.cu", PKG / "csrc" / "planner.cpp"]
 OUT = PKG / "_lib" / "libspotkm.so"
 
 NVCC_FLAGS = [

@@ -426,6 +426,36 @@ def gen_plans(rng):
         except ref_mig.MigrationError:
             doc["error"] = "MigrationError"
         out.append(doc)
+    # missing-source error paths (test_migration.py:222-233 style): wipe every
+    # copy of one layer before planning
+    for t, (o, n) in enumerate([((1, 2, 2), (1, 2, 2)), ((1, 2, 4), (2, 1, 2)), ((2, 2, 1), (1, 4, 1))]):
+        model = ModelSpec(name="e", num_layers=8, bytes_per_layer=1000, kv_bytes_per_token_per_layer=16)
+        old, new = ParallelConfig(*o, 1), ParallelConfig(*n, 1)
+        n_inst = max(old.gpus, new.gpus)
+        instances = [InstanceState(id=f"i-{k}", kind="spot", gpus=1) for k in range(n_inst)]
+        layout = {}
+        for inst, pos in itertools.zip_longest(instances, positions(old)):
+            ref = (inst.id, 0)
+            inv = ContextInventory.empty() if pos is None else required_context(old, pos, model)
+            layout[ref] = ContextInventory(tuple(s for s in inv.model_shards if s[0] != t))
+            inst.gpu_inventories = [layout[ref]]
+        mapping = ref_map.map_devices(instances, new, model, 1)
+        doc = {
+            "model": [model.num_layers, model.bytes_per_layer, model.kv_bytes_per_token_per_layer],
+            "target": list(new.shape()),
+            "assignment": [[g[0], g[1], p.pipeline, p.stage, p.shard] for g, p in mapping.assignment.items()],
+            "old_layout": [[g[0], g[1], enc_inv(inv.model_shards, inv.cache_shards)] for g, inv in layout.items()],
+            "u_max": None, "inherited": None, "departing": [],
+        }
+        try:
+            plan = ref_mig.plan_migration(mapping, layout, model)
+            doc["error"] = None
+            doc["plan"] = ref_mig.plan_to_dict(plan)
+            doc["cost_full"] = hx(ref_cost.migration_cost(plan, _toy_profile(model)))
+        except ref_mig.MigrationError as e:
+            doc["error"] = "MigrationError"
+            doc["message"] = str(e)
+        out.append(doc)
     return out
 
 

@@ -15,12 +15,13 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def header_symbols():
     text = (ROOT / "include" / "spotkm.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sk_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void|double)\s+(sk_\w+)\s*\(",
+                                 text, re.M)))
 
 
 def test_header_declares_expected_symbols():
     syms = header_symbols()
-    assert set(syms) == set(nat.EXPORTS)
+    assert set(syms) == set(nat.EXPORTS) | {"sk_rat_to_double"}
 
 
 def test_library_loads_and_exports_all_symbols():
