@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--all-sizes", action="store_true", help="also report 64..1024 positions")
+    ap.add_argument("--no-reshard", action="store_true", help="skip the N>1 context reshard")
     return ap.parse_args()
 
 
@@ -323,6 +324,101 @@ def kernel_breakdown(runner, flush, reps=2):
     return acc, steps.cpu().numpy().reshape(-1, 2)
 
 
+RESHARD_CASES = {
+    # SURVEY.md 8(d) / BASELINE.md: (geometry, old (D,P,M), new (D,P,M)) per GPU count
+    2: ("llama-30b", (1, 2, 1), (2, 1, 1)),
+    4: ("llama-30b", (1, 2, 2), (1, 1, 4)),
+    8: ("gpt-20b", (1, 2, 4), (2, 1, 4)),
+}
+
+
+class _CudaView:
+    """Zero-copy uint8 view of a raw device range (for the NCCL baseline)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3}
+
+
+def run_reshard(world, rank, local, K=3, W=2, nccl_baseline=True):
+    """Context reshard of BASELINE.json configs[3]/[4] across the world's GPUs:
+    plan from this package's mapper + native planner, executed by k_copy pulls
+    over NVLink (CUDA IPC peer mappings).  Returns the reshard JSON object."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_15566_b200 import reshard
+
+    name, old, new = RESHARD_CASES.get(world, ("gpt-20b", (1, 2, 1), (2, 1, 1)))
+    geom = reshard.LLAMA30B_BF16 if name == "llama-30b" else reshard.GPT20B_BF16
+    plan, layout, need, model, refs = reshard.make_reshard_problem(geom, old, new, 8, 2048)
+    owner = {g: i for i, g in enumerate(refs)}
+    ex = reshard.ReshardExecutor(plan, layout, need, model, owner, rank, world)
+    ex.fill_old()
+    torch.cuda.synchronize()
+    bin_, bout = reshard.traffic(plan)
+    peak_gpu = max(max(bin_.values(), default=0), max(bout.values(), default=0))
+    for _ in range(W):
+        ex.run()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(K):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ex.run()
+        e1.record()
+        e1.synchronize()
+        times.append(allreduce_max(e0.elapsed_time(e1), world))
+    bad = allreduce_sum(float(ex.verify()), world)
+    t = min(times) / 1e3
+    out = {
+        "case": f"{name} bf16 {old}->{new}, KV batch 8 x seq 2048, {world} GPUs",
+        "bytes_total": int(sum(bin_.values())), "bytes_max_gpu": int(peak_gpu),
+        "ms": t * 1e3, "gbs_per_gpu": peak_gpu / t / 1e9,
+        "roofline": {"bound": "nvlink", "peak_nominal_gbs": 900.0, "peak_measured_gbs": 770.0,
+                     "frac_nominal": (peak_gpu / 900e9) / t, "frac_measured": (peak_gpu / 770e9) / t},
+        "byte_identical": bad == 0, "mismatched_words": int(bad),
+        "local_bytes_rank0": ex.local_bytes, "transfers": len(plan.transfers()),
+        "method": "k_copy pull by destination over CUDA-IPC peer mappings, 1 MiB chunks",
+    }
+    if nccl_baseline:
+        # grouped NCCL send/recv of the same transfers (the comparison path)
+        ops = []
+        copies = reshard.plan_copies(plan, layout, need, model)[2]
+        me = refs[rank]
+        for dst, lst in copies.items():
+            for src, soff, doff, n in lst:
+                if src == dst:
+                    continue
+                if src == me:
+                    ops.append(dist.P2POp(dist.isend, torch.as_tensor(
+                        _CudaView(ex.old_mem[me].ptr + soff, n), device="cuda"), owner[dst]))
+                if dst == me:
+                    ops.append(dist.P2POp(dist.irecv, torch.as_tensor(
+                        _CudaView(ex.new_mem[me].ptr + doff, n), device="cuda"), owner[src]))
+        tn = []
+        for it in range(W + K):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if ops:
+                for r in dist.batch_isend_irecv(ops):
+                    r.wait()
+            e1.record()
+            e1.synchronize()
+            if it >= W:
+                tn.append(allreduce_max(e0.elapsed_time(e1), world))
+        out["nccl_grouped_sendrecv_ms"] = min(tn)
+        out["nccl_gbs_per_gpu"] = peak_gpu / (min(tn) / 1e3) / 1e9
+    ex.close()
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -412,6 +508,8 @@ def run_ours(args):
             "value": crate, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{cdone} plans in {cdt:.1f}s; oracle/spotkm_oracle.c (same algorithm in C, "
                       f"OpenMP)"}
+    if world > 1 and not args.no_reshard:
+        line["reshard"] = run_reshard(world, rank, local)
     if args.all_sizes:
         sizes = {}
         for n_pos in (64, 128, 256, 512, 1024):

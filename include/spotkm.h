@@ -176,6 +176,24 @@ int sk_copy_batched(const sk_copy* d_copies, int n_copies, int n_ctas, void* str
 /* Peer-access helper: enable access from `device` to each of `peers`. */
 int sk_enable_peer_access(int device, const int* peers, int n_peers);
 
+/* Executor memory: cudaMalloc'd slabs (exportable with CUDA IPC so peer ranks
+ * of the same box can map them and pull over NVLink). */
+int sk_dev_alloc(uint64_t bytes, void** d_ptr);
+int sk_dev_free(void* d_ptr);
+int sk_ipc_get_handle(const void* d_ptr, void* handle64);   /* 64-byte cudaIpcMemHandle_t */
+int sk_ipc_open_handle(const void* handle64, void** d_ptr);
+int sk_ipc_close_handle(void* d_ptr);
+
+/* Byte-pattern fill / verify of context regions: the 8-byte word at global
+ * byte offset x of a context object holds splitmix64(key ^ x/8).  `base` is
+ * the region's global offset inside its object (8-byte aligned). */
+typedef struct sk_region {
+  uint64_t ptr, bytes, key, base;
+} sk_region;
+int sk_fill_regions(const sk_region* d_regions, int n, void* stream);
+int sk_verify_regions(const sk_region* d_regions, int n, unsigned long long* d_bad, void* stream);
+const char* sk_reshard_error(void);
+
 /* ------------------------------------------------------------------------
  * Migration planner (host, native, bit-exact) -- replaces plan_migration
  * (migration.py:311-384) incl. derive_transfers (201-305), _cover_from_holders

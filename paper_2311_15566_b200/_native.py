@@ -32,6 +32,7 @@ SWEEP_DESC = np.dtype([("oD", "<i4"), ("oP", "<i4"), ("oM", "<i4"), ("G", "<i4")
                        ("alive_off", "<i4"), ("tok_off", "<i4"), ("plan", "<i4"), ("bpl", "<i8"),
                        ("kv", "<i8")], align=True)
 COPY = np.dtype([("src", "<u8"), ("dst", "<u8"), ("bytes", "<u8")], align=True)
+REGION = np.dtype([("ptr", "<u8"), ("bytes", "<u8"), ("key", "<u8"), ("base", "<u8")])
 assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize == 48 and COPY.itemsize == 24
 
 EXPORTS = (
@@ -39,7 +40,9 @@ EXPORTS = (
     "sk_map_outer", "sk_km_dense",
     "sk_sweep_expand", "sk_copy_batched", "sk_enable_peer_access",
     "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
-    "sk_plan_timeline", "sk_memopt_order",
+    "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
+    "sk_ipc_open_handle", "sk_ipc_close_handle", "sk_fill_regions", "sk_verify_regions",
+    "sk_reshard_error",
 )
 
 
@@ -77,6 +80,14 @@ def load():
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),
         "sk_copy_batched": ([vp, i32, i32, vp], i32),
         "sk_enable_peer_access": ([i32, vp, i32], i32),
+        "sk_dev_alloc": ([ctypes.c_uint64, ctypes.POINTER(vp)], i32),
+        "sk_dev_free": ([vp], i32),
+        "sk_ipc_get_handle": ([vp, vp], i32),
+        "sk_ipc_open_handle": ([vp, ctypes.POINTER(vp)], i32),
+        "sk_ipc_close_handle": ([vp], i32),
+        "sk_fill_regions": ([vp, i32, vp], i32),
+        "sk_verify_regions": ([vp, i32, vp, vp], i32),
+        "sk_reshard_error": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

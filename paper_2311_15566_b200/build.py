@@ -15,7 +15,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = [PKG / "csrc" / "spotkm.cu", PKG / "csrc" / "planner.cpp"]
+SRC = [PKG / "csrc" / "spotkm.cu", PKG / "csrc" / "planner.cpp", PKG / "csrc" / "reshard.cu"]
 OUT = PKG / "_lib" / "libspotkm.so"
 
 NVCC_FLAGS = [

@@ -725,7 +725,7 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
       const int4* s4 = reinterpret_cast<const int4*>(src);
       int4* d4 = reinterpret_cast<int4*>(dst);
       uint64_t i = threadIdx.x;
-      constexpr int U = 4;
+      constexpr int U = 8;  // 64 KB in flight per CTA hides NVLink read latency
       for (; i + (U - 1) * kC_TPB < nv; i += U * kC_TPB) {
         int4 t[U];
 #pragma unroll
