@@ -94,7 +94,7 @@ def _find(entries, lo, hi):
 
 def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
     """Per destination GPU: the ordered byte-range copies that realise `plan`
-    (local reuse first, then the plan's transfers in plan order).
+    (the plan's transfers in plan order, then local reuse).
     Returns (old slabs, new slabs, {dst gpu: [(src gpu, src_off, dst_off, bytes)]})."""
     rids = sorted({r for inv in list(old_layout.values()) + list(new_required.values())
                    for r, *_ in inv.cache_shards})
@@ -141,7 +141,10 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
                             X = kv * tok
                             local.append((g, ooff + _span(a - olo, X), off + _span(a - lo, X),
                                           _span(b - a, X)))
-        copies[g] = local + copies[g]
+        # NVLink pulls first (the scarce link), local reuse copies after them:
+        # the copy kernel's CTAs take chunks in list order, so the local HBM
+        # copies fill in behind the remote traffic instead of delaying it
+        copies[g] = copies[g] + local
     return old, new, copies
 
 
