@@ -341,6 +341,20 @@ class _CudaView:
 
 
 def run_reshard(world, rank, local, K=3, W=2, nccl_baseline=True):
+    """Both executor modes (destination pull / source push); the faster is the
+    headline, both are reported."""
+    pull = _reshard_once(world, rank, K, W, "pull", nccl_baseline)
+    push = _reshard_once(world, rank, K, W, "push", False)
+    best = pull if pull["ms"] <= push["ms"] else push
+    out = dict(best)
+    out["modes_ms"] = {"pull": pull["ms"], "push": push["ms"]}
+    if "nccl_grouped_sendrecv_ms" in pull:
+        out["nccl_grouped_sendrecv_ms"] = pull["nccl_grouped_sendrecv_ms"]
+        out["nccl_gbs_per_gpu"] = pull["nccl_gbs_per_gpu"]
+    return out
+
+
+def _reshard_once(world, rank, K, W, mode, nccl_baseline):
     """Context reshard of BASELINE.json configs[3]/[4] across the world's GPUs:
     plan from this package's mapper + native planner, executed by k_copy pulls
     over NVLink (CUDA IPC peer mappings).  Returns the reshard JSON object."""
@@ -353,7 +367,7 @@ def run_reshard(world, rank, local, K=3, W=2, nccl_baseline=True):
     geom = reshard.LLAMA30B_BF16 if name == "llama-30b" else reshard.GPT20B_BF16
     plan, layout, need, model, refs = reshard.make_reshard_problem(geom, old, new, 8, 2048)
     owner = {g: i for i, g in enumerate(refs)}
-    ex = reshard.ReshardExecutor(plan, layout, need, model, owner, rank, world)
+    ex = reshard.ReshardExecutor(plan, layout, need, model, owner, rank, world, mode=mode)
     ex.fill_old()
     torch.cuda.synchronize()
     bin_, bout = reshard.traffic(plan)
@@ -382,7 +396,7 @@ def run_reshard(world, rank, local, K=3, W=2, nccl_baseline=True):
                      "frac_nominal": (peak_gpu / 900e9) / t, "frac_measured": (peak_gpu / 770e9) / t},
         "byte_identical": bad == 0, "mismatched_words": int(bad),
         "local_bytes_rank0": ex.local_bytes, "transfers": len(plan.transfers()),
-        "method": "k_copy pull by destination over CUDA-IPC peer mappings, 1 MiB chunks",
+        "method": f"k_copy {mode} over CUDA-IPC peer mappings, 1 MiB chunks",
     }
     if nccl_baseline:
         # grouped NCCL send/recv of the same transfers (the comparison path)

@@ -184,47 +184,57 @@ class ReshardExecutor:
     """
 
     def __init__(self, plan, old_layout, new_required, model, owner: dict, rank: int = 0,
-                 world: int = 1, seed: int = 1, group=None):
+                 world: int = 1, seed: int = 1, group=None, mode: str = "pull"):
+        if mode not in ("pull", "push"):
+            raise ValueError("mode must be 'pull' or 'push'")
         self.lib = nat.load()
-        self.rank, self.world = rank, world
+        self.rank, self.world, self.mode = rank, world, mode
         self.old, self.new, copies = plan_copies(plan, old_layout, new_required, model, seed)
         self.mine = [g for g, r in owner.items() if r == rank]
         self.old_mem = {g: _Mem(self.old[g].bytes) for g in self.mine if g in self.old}
         self.new_mem = {g: _Mem(self.new[g].bytes) for g in self.mine if g in self.new}
-        self.peer_ptr = {g: m.ptr for g, m in self.old_mem.items()}
+        # device addresses usable from this GPU: own slabs + peer-mapped slabs
+        self.old_ptr = {g: m.ptr for g, m in self.old_mem.items()}
+        self.new_ptr = {g: m.ptr for g, m in self.new_mem.items()}
         self.opened = []
         if world > 1:
             import torch.distributed as dist
 
             handles = {}
-            for g, m in self.old_mem.items():
-                h = ctypes.create_string_buffer(64)
-                nat.check(self.lib.sk_ipc_get_handle(m.ptr, h))
-                handles[g] = h.raw
+            for tag, mems in (("old", self.old_mem), ("new", self.new_mem)):
+                for g, m in mems.items():
+                    h = ctypes.create_string_buffer(64)
+                    nat.check(self.lib.sk_ipc_get_handle(m.ptr, h))
+                    handles[(tag, g)] = h.raw
             gathered = [None] * world
             dist.all_gather_object(gathered, handles, group=group)
             for r, hs in enumerate(gathered):
                 if r == rank:
                     continue
-                for g, raw in hs.items():
+                for (tag, g), raw in hs.items():
+                    if (tag == "old") != (mode == "pull"):
+                        continue   # pull maps peers' old slabs, push their new slabs
                     p = ctypes.c_void_p()
                     nat.check(self.lib.sk_ipc_open_handle(raw, ctypes.byref(p)))
-                    self.peer_ptr[g] = p.value
+                    (self.old_ptr if tag == "old" else self.new_ptr)[g] = p.value
                     self.opened.append(p.value)
+        self.peer_ptr = self.old_ptr
         dev = torch.device("cuda", torch.cuda.current_device())
         rows = []
         self.local_bytes = 0
         self.remote_bytes = 0
-        for g in self.mine:
-            if g not in self.new_mem:
-                continue
-            dbase = self.new_mem[g].ptr
-            for src, soff, doff, n in copies[g]:
-                sbase = self.peer_ptr[src]
-                if src == g:
+        mine = set(self.mine)
+        for dst, lst in copies.items():
+            for src, soff, doff, n in lst:
+                # pull: the destination's rank issues; push: the source's rank
+                issuer = dst if (mode == "pull" or src == dst) else src
+                if issuer not in mine:
+                    continue
+                if src == dst:
                     self.local_bytes += n
                 else:
                     self.remote_bytes += n
+                sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
                 for c in range(0, n, CHUNK):
                     rows.append((sbase + soff + c, dbase + doff + c, min(CHUNK, n - c)))
         arr = np.array(rows, dtype=np.uint64).reshape(-1, 3) if rows else np.zeros((0, 3), np.uint64)
