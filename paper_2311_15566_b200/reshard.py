@@ -53,9 +53,9 @@ def cache_key(seed: int, rid_index: int, layer: int) -> int:
 class Slab:
     """Byte layout of one GPU's context: regions in inventory order."""
 
-    model: dict = field(default_factory=dict)   # layer -> [(lo, hi, offset)]  (lo, hi: Fractions)
-    cache: dict = field(default_factory=dict)   # (rid, layer) -> [(lo, hi, tokens, offset)]
-    regions: list = field(default_factory=list)  # (offset, bytes, key, base)
+    model: dict = field(default_factory=dict)   # layer -> [(lo, hi, where)]  (lo, hi: Fractions)
+    cache: dict = field(default_factory=dict)   # (rid, layer) -> [(lo, hi, tokens, where)]
+    regions: list = field(default_factory=list)  # (where, bytes, key, base); where = (space, offset)
     bytes: int = 0
 
 
@@ -66,21 +66,36 @@ def _span(frac: Fraction, total: int) -> int:
     return v.numerator
 
 
-def build_slab(inv, model, rid_index: dict, seed: int) -> Slab:
+def build_slab(inv, model, rid_index: dict, seed: int, reuse: "Slab | None" = None) -> Slab:
+    """Offsets of an inventory's shards.  With `reuse` (the same GPU's old
+    slab), a shard the GPU already holds EXACTLY is aliased in place
+    (("old", offset): no allocation, no copy); everything else gets space in
+    the new slab (("new", offset))."""
     s = Slab()
     off = 0
     B, kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
     for layer, lo, hi in inv.model_shards:
         a, b = _span(lo, B), _span(hi, B)
-        s.model.setdefault(layer, []).append((lo, hi, off))
-        s.regions.append((off, b - a, model_key(seed, layer), a))
-        off += (b - a + ALIGN - 1) // ALIGN * ALIGN
+        hit = None
+        if reuse is not None:
+            hit = next((e for e in reuse.model.get(layer, ()) if e[0] == lo and e[1] == hi), None)
+        where = ("old", hit[2][1]) if hit else ("new", off)
+        s.model.setdefault(layer, []).append((lo, hi, where))
+        s.regions.append((where, b - a, model_key(seed, layer), a))
+        if not hit:
+            off += (b - a + ALIGN - 1) // ALIGN * ALIGN
     for rid, layer, lo, hi, tok in inv.cache_shards:
         X = kv * tok
         a, b = _span(lo, X), _span(hi, X)
-        s.cache.setdefault((rid, layer), []).append((lo, hi, tok, off))
-        s.regions.append((off, b - a, cache_key(seed, rid_index[rid], layer), a))
-        off += (b - a + ALIGN - 1) // ALIGN * ALIGN
+        hit = None
+        if reuse is not None:
+            hit = next((e for e in reuse.cache.get((rid, layer), ())
+                        if e[0] == lo and e[1] == hi and e[2] == tok), None)
+        where = ("old", hit[3][1]) if hit else ("new", off)
+        s.cache.setdefault((rid, layer), []).append((lo, hi, tok, where))
+        s.regions.append((where, b - a, cache_key(seed, rid_index[rid], layer), a))
+        if not hit:
+            off += (b - a + ALIGN - 1) // ALIGN * ALIGN
     s.bytes = off
     return s
 
@@ -100,7 +115,7 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
                    for r, *_ in inv.cache_shards})
     rid_index = {r: i for i, r in enumerate(rids)}
     old = {g: build_slab(inv, model, rid_index, seed) for g, inv in old_layout.items()}
-    new = {g: build_slab(inv, model, rid_index, seed) for g, inv in new_required.items()}
+    new = {g: build_slab(inv, model, rid_index, seed, old.get(g)) for g, inv in new_required.items()}
     B, kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
     copies: dict = {g: [] for g in new}
     for action in plan.actions:
@@ -119,23 +134,29 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
             n = _span(t.hi - t.lo, unit)
             if n != t.bytes:
                 raise ValueError(f"transfer bytes {t.bytes} != geometry {n}")
-            copies[t.dst].append((t.src, src[-1] + _span(t.lo - src[0], unit),
-                                  dst[-1] + _span(t.lo - dst[0], unit), n))
+            if dst[-1][0] != "new":
+                raise ValueError(f"transfer {t} targets a shard its destination already holds")
+            copies[t.dst].append((t.src, src[-1][1] + _span(t.lo - src[0], unit),
+                                  dst[-1][1] + _span(t.lo - dst[0], unit), n))
     # local reuse: every needed piece the GPU already holds (the plan's "kept" bytes)
     for g, slab in new.items():
         have = old.get(g)
         local = []
         if have is not None:
             for layer, ents in slab.model.items():
-                for lo, hi, off in ents:
-                    for olo, ohi, ooff in have.model.get(layer, ()):
+                for lo, hi, (space, off) in ents:
+                    if space != "new":
+                        continue   # aliased in place: nothing to move
+                    for olo, ohi, (_, ooff) in have.model.get(layer, ()):
                         a, b = max(lo, olo), min(hi, ohi)
                         if b > a:
                             local.append((g, ooff + _span(a - olo, B), off + _span(a - lo, B),
                                           _span(b - a, B)))
             for key, ents in slab.cache.items():
-                for lo, hi, tok, off in ents:
-                    for olo, ohi, otok, ooff in have.cache.get(key, ()):
+                for lo, hi, tok, (space, off) in ents:
+                    if space != "new":
+                        continue
+                    for olo, ohi, otok, (_, ooff) in have.cache.get(key, ()):
                         a, b = max(lo, olo), min(hi, ohi)
                         if b > a and otok == tok:
                             X = kv * tok
@@ -243,16 +264,18 @@ class ReshardExecutor:
             cp["src"], cp["dst"], cp["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
         self.n_copies = len(cp)
         self.d_copies = torch.from_numpy(cp.view(np.uint8)).to(dev) if len(cp) else None
-        self.d_fill = self._regions(self.old, self.old_mem, dev)
-        self.d_check = self._regions(self.new, self.new_mem, dev)
+        self.d_fill = self._regions(self.old, self.old_mem, self.old_mem, dev)
+        self.d_check = self._regions(self.new, self.new_mem, self.old_mem, dev)
         self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
 
     @staticmethod
-    def _regions(slabs, mems, dev):
+    def _regions(slabs, mems, old_mems, dev):
         rows = []
         for g, m in mems.items():
-            for off, n, key, base in slabs[g].regions:
-                rows.append((m.ptr + off, n, key, base))
+            for where, n, key, base in slabs[g].regions:
+                space, off = where
+                ptr = (m.ptr if space == "new" else old_mems[g].ptr) + off
+                rows.append((ptr, n, key, base))
         reg = np.zeros(len(rows), dtype=nat.REGION)
         for i, r in enumerate(rows):
             reg[i] = r
