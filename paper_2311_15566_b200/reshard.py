@@ -169,6 +169,18 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
     return old, new, copies
 
 
+def issue_lists(copies: dict, owner: dict, mode: str = "pull") -> dict:
+    """Which rank issues which copy: pull -> the destination GPU's rank, push ->
+    the source GPU's rank; local (same-GPU) copies always by the owner.
+    Returns {rank: [(src, dst, src_off, dst_off, bytes)]} in plan order."""
+    out: dict = {}
+    for dst, lst in copies.items():
+        for src, soff, doff, n in lst:
+            issuer = dst if (mode == "pull" or src == dst) else src
+            out.setdefault(owner[issuer], []).append((src, dst, soff, doff, n))
+    return out
+
+
 def traffic(plan):
     """bytes in / out per GPU over NVLink (src != dst GPU)."""
     bin_, bout = {}, {}
@@ -244,20 +256,14 @@ class ReshardExecutor:
         rows = []
         self.local_bytes = 0
         self.remote_bytes = 0
-        mine = set(self.mine)
-        for dst, lst in copies.items():
-            for src, soff, doff, n in lst:
-                # pull: the destination's rank issues; push: the source's rank
-                issuer = dst if (mode == "pull" or src == dst) else src
-                if issuer not in mine:
-                    continue
-                if src == dst:
-                    self.local_bytes += n
-                else:
-                    self.remote_bytes += n
-                sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
-                for c in range(0, n, CHUNK):
-                    rows.append((sbase + soff + c, dbase + doff + c, min(CHUNK, n - c)))
+        for src, dst, soff, doff, n in issue_lists(copies, owner, mode).get(rank, ()):
+            if src == dst:
+                self.local_bytes += n
+            else:
+                self.remote_bytes += n
+            sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
+            for c in range(0, n, CHUNK):
+                rows.append((sbase + soff + c, dbase + doff + c, min(CHUNK, n - c)))
         arr = np.array(rows, dtype=np.uint64).reshape(-1, 3) if rows else np.zeros((0, 3), np.uint64)
         cp = np.zeros(len(arr), dtype=nat.COPY)
         if len(arr):
