@@ -68,7 +68,7 @@ def _span(frac: Fraction, total: int) -> int:
 
 def build_slab(inv, model, rid_index: dict, seed: int, reuse: "Slab | None" = None) -> Slab:
     """Offsets of an inventory's shards.  With `reuse` (the same GPU's old
-    slab), a shard the GPU already holds EXACTLY is aliased in place
+    slab), a shard contained in one the GPU already holds is aliased in place
     (("old", offset): no allocation, no copy); everything else gets space in
     the new slab (("new", offset))."""
     s = Slab()
@@ -78,8 +78,8 @@ def build_slab(inv, model, rid_index: dict, seed: int, reuse: "Slab | None" = No
         a, b = _span(lo, B), _span(hi, B)
         hit = None
         if reuse is not None:
-            hit = next((e for e in reuse.model.get(layer, ()) if e[0] == lo and e[1] == hi), None)
-        where = ("old", hit[2][1]) if hit else ("new", off)
+            hit = next((e for e in reuse.model.get(layer, ()) if e[0] <= lo and hi <= e[1]), None)
+        where = ("old", hit[2][1] + _span(lo - hit[0], B)) if hit else ("new", off)
         s.model.setdefault(layer, []).append((lo, hi, where))
         s.regions.append((where, b - a, model_key(seed, layer), a))
         if not hit:
@@ -90,8 +90,8 @@ def build_slab(inv, model, rid_index: dict, seed: int, reuse: "Slab | None" = No
         hit = None
         if reuse is not None:
             hit = next((e for e in reuse.cache.get((rid, layer), ())
-                        if e[0] == lo and e[1] == hi and e[2] == tok), None)
-        where = ("old", hit[3][1]) if hit else ("new", off)
+                        if e[0] <= lo and hi <= e[1] and e[2] == tok), None)
+        where = ("old", hit[3][1] + _span(lo - hit[0], X)) if hit else ("new", off)
         s.cache.setdefault((rid, layer), []).append((lo, hi, tok, where))
         s.regions.append((where, b - a, cache_key(seed, rid_index[rid], layer), a))
         if not hit:
