@@ -111,12 +111,12 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
  *   d_perm  : >= sum over plans of nA*nB uint32    (scratch, at f_off)
  *   d_assign: per plan R int32 at out_off: column index or -1 (unassigned)
  *   d_total : per plan total_weight (accumulated in the reference order)
- *   max_pairs = max nA*nB, max_n = max(nA, nB), max_rows = max R over the batch.
+ *   max_na / max_nb = max fused rows / slots (R/g, C/g), max_rows = max R over the batch.
  *   group_mask: bit g set when some plan has group g (0 = any of 1..8).
  */
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm,
-                   int32_t* d_assign, double* d_total, int64_t max_pairs, int max_n,
+                   int32_t* d_assign, double* d_total, int max_na, int max_nb,
                    int max_rows, int group_mask, void* stream);
 
 /* The two halves of sk_map_batched, for callers that time or pipeline them:
@@ -124,7 +124,7 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
  * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element
  * loads} (2 x int64) -- the algorithmic work of the outer KM. */
 int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
-                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int64_t max_pairs,
+                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na, int max_nb,
                 int group_mask, void* stream);
 int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                  const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,

@@ -245,17 +245,14 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
 // ---------------------------------------------------------------------------
 // K2a: per fused pair (a, b): g x g block -> inner KM -> fused weight + perm
 
-constexpr int kF_TPB = 128;
-constexpr int kF_PPT = 1;  // fused pairs per thread
 
 template <int G>
-__device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB,
+__device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB, const Col c0,
                                           const int32_t* __restrict__ row_ptr,
                                           const sk_segment* __restrict__ segs,
                                           double* __restrict__ F, uint32_t* __restrict__ perm_out,
                                           uint32_t zero_perm) {
-  // the G columns of fused slot b share (pipeline, stage): one decode
-  const Col c0 = col_of(p, b * G);
+  // the G columns of fused slot b share (pipeline, stage): c0 is their decode
   const int wdt = c0.i1 - c0.i0;
   long long num[G][G];
   long long any = 0;
@@ -322,6 +319,10 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
   perm_out[idx] = packed;
 }
 
+// One thread per fused pair, pairs linear in (a, b) with b fastest: a warp's
+// lanes share their row group (broadcast segment loads).
+constexpr int kF_TPB = 128;
+
 template <int G>
 __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
                                                  const int32_t* __restrict__ row_ptr,
@@ -332,14 +333,10 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   if (p.group != G) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
-  const long long total = (long long)nA * nB;
-  const long long base = (long long)blockIdx.x * (kF_TPB * kF_PPT) + threadIdx.x;
-#pragma unroll
-  for (int i = 0; i < kF_PPT; ++i) {
-    const long long pair = base + (long long)i * kF_TPB;
-    if (pair < total)
-      fuse_pair<G>(p, (int)(pair / nB), (int)(pair % nB), nB, row_ptr, segs, F, perm, zero_perm);
-  }
+  const long long pair = (long long)blockIdx.x * kF_TPB + threadIdx.x;
+  if (pair >= (long long)nA * nB) return;
+  const int a = (int)(pair / nB), b = (int)(pair % nB);
+  fuse_pair<G>(p, a, b, nB, col_of(p, b * G), row_ptr, segs, F, perm, zero_perm);
 }
 
 // The inner KM's answer on an all-zero g x g block, replayed once on the host
@@ -357,10 +354,10 @@ uint32_t zero_block_perm() {
 }
 
 template <int G>
-int launch_fuse(const sk_plan* d_plans, int p0, int np, long long max_pairs, const int32_t* row_ptr,
+int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
   static const uint32_t zp = zero_block_perm<G>();
-  const long long bx = (max_pairs + kF_TPB * kF_PPT - 1) / (kF_TPB * kF_PPT);
+  const long long bx = ((long long)max_na * max_nb + kF_TPB - 1) / kF_TPB;
   dim3 grid((unsigned)bx, np);
   k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
   return cuda_check("k_fuse launch");
@@ -824,24 +821,25 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
 }
 
 int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
-                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int64_t max_pairs,
+                const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na, int max_nb,
                 int group_mask, void* stream) {
-  if (n_plans < 0 || max_pairs < 0) return set_err(SK_EINVAL, "negative sizes");
-  if (n_plans == 0 || max_pairs == 0) return SK_OK;
-  if ((max_pairs + kF_TPB - 1) / kF_TPB > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
+  if (n_plans < 0 || max_na < 0 || max_nb < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0 || max_na == 0 || max_nb == 0) return SK_OK;
+  if (((long long)max_na * max_nb + kF_TPB - 1) / kF_TPB > 0x7fffffffLL)
+    return set_err(SK_EINVAL, "too many fused pairs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int mask = group_mask ? group_mask : 0x1fe;
   for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
     const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
     int rc = SK_OK;
-    if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 4))) rc = launch_fuse<4>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 5))) rc = launch_fuse<5>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 6))) rc = launch_fuse<6>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 7))) rc = launch_fuse<7>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
-    if (!rc && (mask & (1 << 8))) rc = launch_fuse<8>(d_plans, p0, np, max_pairs, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 4))) rc = launch_fuse<4>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 5))) rc = launch_fuse<5>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 6))) rc = launch_fuse<6>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 7))) rc = launch_fuse<7>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
+    if (!rc && (mask & (1 << 8))) rc = launch_fuse<8>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
     if (rc) return rc;
   }
   return SK_OK;
@@ -859,10 +857,12 @@ int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
 
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int32_t* d_assign,
-                   double* d_total, int64_t max_pairs, int max_n, int max_rows, int group_mask,
+                   double* d_total, int max_na, int max_nb, int max_rows, int group_mask,
                    void* stream) {
-  int rc = sk_map_fuse(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, max_pairs, group_mask, stream);
+  int rc = sk_map_fuse(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, max_na, max_nb,
+                       group_mask, stream);
   if (rc) return rc;
+  const int max_n = max_na > max_nb ? max_na : max_nb;
   return sk_map_outer(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, nullptr,
                       max_n, max_rows, stream);
 }

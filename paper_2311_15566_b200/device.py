@@ -52,7 +52,7 @@ class MapBatch:
         plans = np.zeros(Q, dtype=nat.PLAN)
         seg_base = row_base = f_off = out_off = 0
         rp_parts = []
-        max_pairs = max_n = max_rows = max_cols = 0
+        max_pairs = max_n = max_rows = max_cols = max_na = max_nb = 0
         gmask = 0
         seg_parts = []
         for slot, q in enumerate(order):
@@ -69,6 +69,8 @@ class MapBatch:
             out_off += R
             max_pairs = max(max_pairs, nA * nB)
             max_n = max(max_n, nA, nB)
+            max_na = max(max_na, nA)
+            max_nb = max(max_nb, nB)
             max_rows = max(max_rows, R)
             max_cols = max(max_cols, C)
             gmask |= 1 << g
@@ -76,6 +78,7 @@ class MapBatch:
         row_ptr = np.concatenate(rp_parts).astype(np.int32)
         segs = np.concatenate(seg_parts) if seg_parts else np.zeros(0, dtype=nat.SEGMENT)
         info = dict(Q=Q, rows=row_base, pairs=f_off, max_pairs=max_pairs, max_n=max_n,
+                    max_na=max_na, max_nb=max_nb,
                     max_rows=max_rows, max_cols=max_cols, gmask=gmask)
         return plans, row_ptr, segs, info
 
@@ -116,7 +119,7 @@ class MapBatch:
         p_assign = p_total + 8 * Q
         st = _stream_ptr()
         rc = lib.sk_map_fuse(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
-                             info["max_pairs"], info["gmask"], st)
+                             info["max_na"], info["max_nb"], info["gmask"], st)
         nat.check(rc, mapping_error)
         ns = np.array([n_of[q] for q in order], dtype=np.int64)
         for a, b, mn in outer_classes(ns):

@@ -184,7 +184,8 @@ class SweepRunner:
         self.max_n = int(st["n"].max())
         self.classes = outer_classes(st["n"])
         self.class_rows = [int(st["rows"][a:b].max()) for a, b, _ in self.classes]
-        self.class_pairs = [int(st["pairs"][a:b].max()) for a, b, _ in self.classes]
+        self.class_na = [int(st["nA"][a:b].max()) for a, b, _ in self.classes]
+        self.class_nb = [int(st["nB"][a:b].max()) for a, b, _ in self.classes]
         self.class_gmask = [int(np.bitwise_or.reduce(1 << batch.plans["group"][a:b].astype(np.int64)))
                             for a, b, _ in self.classes]
         self.max_rows = int(st["rows"].max())
@@ -258,7 +259,7 @@ class SweepRunner:
                 st = main
             rc = self.lib.sk_map_fuse(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
                                       self.segs.data_ptr(), self.fused.data_ptr(),
-                                      self.perm.data_ptr(), self.class_pairs[c],
+                                      self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
                                       self.class_gmask[c], st.cuda_stream)
             nat.check(rc)
             mark("k_fuse")
