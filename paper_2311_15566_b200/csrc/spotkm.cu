@@ -419,6 +419,20 @@ struct OuterArgs {
   int dbl_elems;
 };
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ unsigned lds_u8(unsigned a) {
+  unsigned v;
+  asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
 __device__ __forceinline__ unsigned long long order_key(double x) {
   const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
@@ -447,11 +461,13 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   const double* Fp = A.F + p.f_off;
   // dictionary-code the fused matrix into shared memory (CODED variant)
   bool coded = false;
-  unsigned long long* table = nullptr;
-  unsigned char* codes = nullptr;
+  // (pointers derived unconditionally from the __shared__ array so the
+  // compiler addresses them as shared memory: plain LDS, no generic windows)
+  unsigned long long* table =
+      reinterpret_cast<unsigned long long*>(base + outer_base_bytes(A.max_n, A.dbl_elems));
+  unsigned char* codes = reinterpret_cast<unsigned char*>(table + kDictSlots);
+  const unsigned table_s = smem_addr(table), codes_s = smem_addr(codes);
   if (CODED) {
-    table = reinterpret_cast<unsigned long long*>(base + outer_base_bytes(A.max_n, A.dbl_elems));
-    codes = reinterpret_cast<unsigned char*>(table + kDictSlots);
     for (int t = lane; t < kDictSlots; t += 32) table[t] = kEmpty;
     __syncwarp();
     bool fail = false;
@@ -532,11 +548,12 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       const long long rowo = (long long)(i0 - 1) * nB - 1;
       double cst[CPL];
       if (CODED && coded) {
-        const unsigned char* rowc = codes + rowo;
+        // 32-bit shared-window addresses: one LDS.U8 + one LDS.64 per column
+        const unsigned rowc = codes_s + (unsigned)((int)rowo + lane);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
-          if ((ld >> k) & 1ull) x = __longlong_as_double((long long)table[rowc[lane + 32 * k]]);
+          if ((ld >> k) & 1ull) x = lds_f64(table_s + 8u * lds_u8(rowc + 32u * k));
           cst[k] = -x;
         }
       } else {
