@@ -398,9 +398,11 @@ __host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int max_r
   size_t bytes = (size_t)outer_dbl_elems(max_n, max_rows) * 8 + (size_t)(max_n + 1) * 4 * 2;
   return (bytes + 15) & ~(size_t)15;
 }
-__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, bool coded) {
+__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, bool coded,
+                                                              int warps = 1) {
   size_t bytes = outer_base_bytes(max_n, max_rows);
   if (coded) bytes += (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + 15) & ~(size_t)15);
+  if (warps > 1) bytes += (size_t)2 * warps * 24;  // step partials (key, value, j)
   return bytes;
 }
 
@@ -438,12 +440,27 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-template <int CPL, bool CODED>
+// W = warps per plan.  W == 1: one warp per plan, several plans per block,
+// warp-synchronous (the common case: many plans, small n).  W > 1: one block
+// per plan, columns spread over W warps, one __syncthreads per Dijkstra step
+// (the warp winners are combined through double-buffered shared partials) --
+// for big plans (n >~ 250) where per-plan latency, not throughput, binds.
+template <int W>
+__device__ __forceinline__ void plan_sync() {
+  if (W == 1)
+    __syncwarp();
+  else
+    __syncthreads();
+}
+
+template <int CPL, bool CODED, int W>
 __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (q >= A.n_plans) return;
+  constexpr int T = 32 * W;  // threads per plan
+  const int pt = threadIdx.x % T, slot = threadIdx.x / T;
+  const int lane = threadIdx.x & 31, pw = pt >> 5;
+  const int q = blockIdx.x * (blockDim.x / T) + slot;
+  if (q >= A.n_plans) return;  // uniform per plan (W > 1: per block)
   const sk_plan p = A.plans[q];
   const int g = p.group;
   const bool dense = (p.flags & SK_PLAN_DENSE) != 0;
@@ -452,37 +469,46 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   const int n = nA > nB ? nA : nB;
   const int n1 = A.max_n + 1;
 
-  // per-warp layout: [double ucol / wv: dbl_elems] [int match: n1] [int way: n1]
-  unsigned char* base = smem + (size_t)warp * A.smem_per_warp;
+  // per-plan layout: [double ucol / wv: dbl_elems] [int match: n1] [int way: n1]
+  //                  [CODED: u64 table[256] | u8 codes[max_n^2]] ; W > 1 partials after
+  unsigned char* base = smem + (size_t)slot * A.smem_per_warp;
   double* ucol = reinterpret_cast<double*>(base);
   int* match = reinterpret_cast<int*>(base + (size_t)A.dbl_elems * 8);
   int* way = match + n1;
 
   const double* Fp = A.F + p.f_off;
-  // dictionary-code the fused matrix into shared memory (CODED variant)
-  bool coded = false;
+  // dictionary-code the fused matrix into shared memory (CODED variant).
   // (pointers derived unconditionally from the __shared__ array so the
   // compiler addresses them as shared memory: plain LDS, no generic windows)
+  bool coded = false;
   unsigned long long* table =
       reinterpret_cast<unsigned long long*>(base + outer_base_bytes(A.max_n, A.dbl_elems));
   unsigned char* codes = reinterpret_cast<unsigned char*>(table + kDictSlots);
   const unsigned table_s = smem_addr(table), codes_s = smem_addr(codes);
+  // W > 1: warp-winner partials, double-buffered by step parity
+  struct Partial {
+    unsigned long long key;
+    double val;
+    unsigned j, pad;
+  };
+  Partial* partial = reinterpret_cast<Partial*>(
+      base + (A.smem_per_warp - (size_t)2 * W * sizeof(Partial)));
   if (CODED) {
-    for (int t = lane; t < kDictSlots; t += 32) table[t] = kEmpty;
-    __syncwarp();
+    for (int t = pt; t < kDictSlots; t += T) table[t] = kEmpty;
+    plan_sync<W>();
     bool fail = false;
     const int cnt = nA * nB;
-    constexpr int U = 8;  // independent loads in flight per lane
-    for (int e0 = 0; e0 < cnt; e0 += 32 * U) {
+    constexpr int U = 8;  // independent loads in flight per thread
+    for (int e0 = 0; e0 < cnt; e0 += T * U) {
       unsigned long long bits[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 32 + lane;
+        const int e = e0 + u * T + pt;
         bits[u] = e < cnt ? (unsigned long long)__double_as_longlong(__ldg(Fp + e)) : kEmpty;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * 32 + lane;
+        const int e = e0 + u * T + pt;
         // one insert per distinct value per warp: the lowest lane holding it
         const unsigned peers = __match_any_sync(kFull, bits[u]);
         const int leader = __ffs(peers) - 1;
@@ -503,15 +529,19 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
         if (e < cnt) codes[e] = (unsigned char)h;
       }
     }
-    coded = !__any_sync(kFull, fail);
-    __syncwarp();
+    if (W == 1) {
+      coded = !__any_sync(kFull, fail);
+      __syncwarp();
+    } else {
+      coded = !__syncthreads_or(fail);
+    }
   }
 
   // static column masks: valid = 1..n, real = 1..nB (beyond: zero padding)
   unsigned long long valid = 0ull, real = 0ull;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
-    const int j = lane + 32 * k;
+    const int j = pt + T * k;
     if (j >= 1 && j <= n) valid |= 1ull << k;
     if (j >= 1 && j <= nB) real |= 1ull << k;
   }
@@ -522,22 +552,20 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
     v[k] = 0.0;
     wr[k] = 0;
   }
-  for (int j = lane; j <= n; j += 32) {
+  for (int j = pt; j <= n; j += T) {
     ucol[j] = 0.0;
     match[j] = 0;
   }
-  __syncwarp();
+  plan_sync<W>();
+  if (pt == 0) match[0] = 1;  // row 1 (ucol[0] = 0.0 already)
+  plan_sync<W>();
 
   long long nsteps = 0, nloads = 0;
+  int parity = 0;
   for (int i = 1; i <= n; ++i) {
-    if (lane == 0) {
-      match[0] = i;
-      ucol[0] = 0.0;
-    }
-    unsigned long long used = (lane == 0) ? 1ull : 0ull;  // column 0
+    unsigned long long used = (pt == 0) ? 1ull : 0ull;  // column 0
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
-    __syncwarp();
     int j0 = 0;
     while (true) {
       ++nsteps;
@@ -549,19 +577,19 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       double cst[CPL];
       if (CODED && coded) {
         // 32-bit shared-window addresses: one LDS.U8 + one LDS.64 per column
-        const unsigned rowc = codes_s + (unsigned)((int)rowo + lane);
+        const unsigned rowc = codes_s + (unsigned)((int)rowo + pt);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
-          if ((ld >> k) & 1ull) x = lds_f64(table_s + 8u * lds_u8(rowc + 32u * k));
+          if ((ld >> k) & 1ull) x = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
           cst[k] = -x;
         }
       } else {
-        const double* rowp = Fp + rowo;
+        const double* rowp = Fp + rowo + pt;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
-          if ((ld >> k) & 1ull) x = __ldg(rowp + lane + 32 * k);
+          if ((ld >> k) & 1ull) x = __ldg(rowp + T * k);
           cst[k] = -x;
         }
       }
@@ -580,14 +608,34 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
         best = better ? mk : best;
         bk = better ? k : bk;
       }
-      const unsigned bj = (best < kInf) ? (unsigned)(lane + 32 * bk) : 0xffffffffu;
+      // argmin over (value, lowest j): order-preserving key, three redux.sync
+      const unsigned bj = (best < kInf) ? (unsigned)(pt + T * bk) : 0xffffffffu;
       const unsigned long long key = order_key(best);
       const unsigned hi = __reduce_min_sync(kFull, (unsigned)(key >> 32));
       const bool c1 = (unsigned)(key >> 32) == hi;
       const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
       const bool c2 = c1 && (unsigned)key == lo;
-      const int j1 = (int)__reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
-      const double delta = __shfl_sync(kFull, best, j1 & 31);
+      unsigned jw = __reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
+      double delta = __shfl_sync(kFull, best, (jw % T) & 31);
+      if (W > 1) {
+        Partial* pp = partial + parity * W;
+        if (lane == 0) pp[pw] = {((unsigned long long)hi << 32) | lo, delta, jw, 0u};
+        __syncthreads();
+        unsigned long long bkey = pp[0].key;
+        jw = pp[0].j;
+        delta = pp[0].val;
+#pragma unroll
+        for (int w = 1; w < W; ++w) {
+          const Partial o = pp[w];
+          if (o.key < bkey || (o.key == bkey && o.j < jw)) {
+            bkey = o.key;
+            jw = o.j;
+            delta = o.val;
+          }
+        }
+        parity ^= 1;
+      }
+      const int j1 = (int)jw;
       // a zero delta leaves every potential and slack numerically unchanged
       // (at most flips the sign of a zero, which no comparison or later
       // non-zero result can observe), so the update is skipped
@@ -595,42 +643,45 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           const bool u = (used >> k) & 1ull;
-          if (u) ucol[lane + 32 * k] += delta;
+          if (u) ucol[pt + T * k] += delta;
           v[k] = u ? v[k] - delta : v[k];
           minv[k] = (!u && ((valid >> k) & 1ull)) ? minv[k] - delta : minv[k];
         }
       }
       j0 = j1;
-      if ((j0 & 31) == lane) used |= 1ull << (j0 >> 5);
+      if (j0 % T == pt) used |= 1ull << (j0 / T);
       if (match[j0] == 0) break;
     }
-    // publish predecessors, then walk the augmenting path (lane 0)
+    // publish predecessors, then walk the augmenting path (one thread), then
+    // seed the next row
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
-      if (((used | valid) >> k) & 1ull) way[lane + 32 * k] = wr[k];
-    __syncwarp();
-    if (lane == 0) {
+      if (((used | valid) >> k) & 1ull) way[pt + T * k] = wr[k];
+    plan_sync<W>();
+    if (pt == 0) {
       while (j0) {
         const int j1 = way[j0];
         match[j0] = match[j1];
         ucol[j0] = ucol[j1];
         j0 = j1;
       }
+      match[0] = i + 1;
+      ucol[0] = 0.0;
     }
-    __syncwarp();
+    plan_sync<W>();
   }
 
   // row_to_col for real fused rows -> way[] (free now)
-  for (int j = lane + 1; j <= n; j += 32) {
+  for (int j = pt + 1; j <= n; j += T) {
     const int r = match[j];
     if (r >= 1 && r <= nA) way[r - 1] = j - 1;
   }
-  __syncwarp();
+  plan_sync<W>();
   double* wv = ucol;
   int32_t* out = A.assign + p.out_off;
   const int32_t* __restrict__ row_ptr = A.row_ptr;
   const sk_segment* __restrict__ segs = A.segs;
-  for (int r = lane; r < p.rows; r += 32) {
+  for (int r = pt; r < p.rows; r += T) {
     const int a = r / g, k = r % g;
     const int b = way[a];
     if (b < nB) {
@@ -644,16 +695,21 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       wv[r] = -1.0;
     }
   }
-  __syncwarp();
+  plan_sync<W>();
   if (A.steps) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);
-    if (lane == 0) {
-      A.steps[2 * q] = nsteps;
-      A.steps[2 * q + 1] = nloads;
+    if (pt == 0) A.steps[2 * q] = nsteps;
+    if (W == 1) {
+      if (lane == 0) A.steps[2 * q + 1] = nloads;
+    } else {
+      if (pt == 0) A.steps[2 * q + 1] = 0;
+      __syncthreads();
+      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A.steps + 2 * q + 1),
+                               (unsigned long long)nloads);
     }
   }
-  if (lane == 0) {
+  if (pt == 0) {
     // total_weight in the reference's order (mapping.py:143-148 / 274-282)
     double t = 0.0;
     for (int r = 0; r < p.rows; ++r) {
@@ -754,57 +810,61 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
   }
 }
 
-template <int CPL>
+template <int CPL, int W>
 int launch_outer(OuterArgs A, int max_rows, cudaStream_t s) {
   A.dbl_elems = outer_dbl_elems(A.max_n, max_rows);
   constexpr size_t kSmemCap = 200 * 1024;
-  // coded variant when a block of >= 2 warps fits; fewer warps per block for
-  // big plans so the codes still fit
-  const size_t coded_warp = outer_smem_per_warp(A.max_n, max_rows, true);
-  int warps = kO_WARPS;
+  // coded variant when it fits; W == 1 packs up to kO_WARPS plans per block
+  // (fewer for big plans so the codes still fit)
+  const size_t coded_plan = outer_smem_per_warp(A.max_n, max_rows, true, W);
+  int per_block = W == 1 ? kO_WARPS : 1;
   bool coded = true;
-  while (warps > 1 && coded_warp * warps > kSmemCap) --warps;
-  if (coded_warp * warps > kSmemCap) {
+  while (per_block > 1 && coded_plan * per_block > kSmemCap) --per_block;
+  if (coded_plan * per_block > kSmemCap) {
     coded = false;
-    warps = kO_WARPS;
+    per_block = W == 1 ? kO_WARPS : 1;
   }
-  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows, coded);
-  const size_t smem = A.smem_per_warp * warps;
+  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows, coded, W);
+  const size_t smem = A.smem_per_warp * per_block;
   if (smem > 227 * 1024) return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", smem);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(k_outer<CPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_outer<CPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_outer<CPL, true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_outer<CPL, false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     configured = true;
   }
-  const int blocks = (A.n_plans + warps - 1) / warps;
+  const int blocks = (A.n_plans + per_block - 1) / per_block;
   if (coded)
-    k_outer<CPL, true><<<blocks, warps * 32, smem, s>>>(A);
+    k_outer<CPL, true, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
   else
-    k_outer<CPL, false><<<blocks, warps * 32, smem, s>>>(A);
+    k_outer<CPL, false, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
   return cuda_check("k_outer launch");
 }
 
+// Small plans: one warp per plan (columns per lane = need).  Big plans
+// (more than 8 columns per lane): one 4-warp block per plan.
 int outer_dispatch(const OuterArgs& A, int max_rows, cudaStream_t s) {
-  const int need = (A.max_n + 1 + 31) / 32;  // columns per lane
+  const int need = (A.max_n + 1 + 31) / 32;  // columns per lane with one warp
   switch (need) {
     case 0:
-    case 1: return launch_outer<1>(A, max_rows, s);
-    case 2: return launch_outer<2>(A, max_rows, s);
-    case 3: return launch_outer<3>(A, max_rows, s);
-    case 4: return launch_outer<4>(A, max_rows, s);
-    case 5: return launch_outer<5>(A, max_rows, s);
-    case 6: return launch_outer<6>(A, max_rows, s);
+    case 1: return launch_outer<1, 1>(A, max_rows, s);
+    case 2: return launch_outer<2, 1>(A, max_rows, s);
+    case 3: return launch_outer<3, 1>(A, max_rows, s);
+    case 4: return launch_outer<4, 1>(A, max_rows, s);
+    case 5: return launch_outer<5, 1>(A, max_rows, s);
+    case 6: return launch_outer<6, 1>(A, max_rows, s);
     case 7:
-    case 8: return launch_outer<8>(A, max_rows, s);
+    case 8: return launch_outer<8, 1>(A, max_rows, s);
     default: break;
   }
-  if (need <= 12) return launch_outer<12>(A, max_rows, s);
-  if (need <= 17) return launch_outer<17>(A, max_rows, s);
-  if (need <= 24) return launch_outer<24>(A, max_rows, s);
-  if (need <= 33) return launch_outer<33>(A, max_rows, s);
-  if (need <= 48) return launch_outer<48>(A, max_rows, s);
-  if (need <= 64) return launch_outer<64>(A, max_rows, s);
+  const int need4 = (A.max_n + 1 + 127) / 128;  // columns per thread with 4 warps
+  if (need4 <= 3) return launch_outer<3, 4>(A, max_rows, s);
+  if (need4 <= 4) return launch_outer<4, 4>(A, max_rows, s);
+  if (need4 <= 5) return launch_outer<5, 4>(A, max_rows, s);
+  if (need4 <= 6) return launch_outer<6, 4>(A, max_rows, s);
+  if (need4 <= 8) return launch_outer<8, 4>(A, max_rows, s);
+  if (need4 <= 12) return launch_outer<12, 4>(A, max_rows, s);
+  if (need4 <= 16) return launch_outer<16, 4>(A, max_rows, s);
   return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", A.max_n);
 }
 

@@ -138,17 +138,19 @@ def _align(n: int, a: int = 256) -> int:
     return (n + a - 1) // a * a
 
 
-_CPL_BUCKETS = (1, 2, 3, 4, 5, 6, 8, 8, 12, 12, 12, 12, 17, 17, 17, 17, 17, 24, 24, 24, 24, 24, 24,
-                24, 33, 33, 33, 33, 33, 33, 33, 33, 33)
-
-
-def cpl_bucket(n: int) -> int:
-    """Columns-per-lane template the outer-KM dispatch picks for size n
-    (mirrors outer_dispatch in spotkm.cu)."""
+def cpl_bucket(n: int):
+    """(warps per plan, columns per thread) of the outer-KM template the
+    dispatch picks for size n (mirrors outer_dispatch in spotkm.cu)."""
     need = max(1, (n + 1 + 31) // 32)
-    if need <= len(_CPL_BUCKETS):
-        return _CPL_BUCKETS[need - 1]
-    return 48 if need <= 48 else 64
+    if need <= 6:
+        return (1, need)
+    if need <= 8:
+        return (1, 8)
+    need4 = (n + 1 + 127) // 128
+    for c in (3, 4, 5, 6, 8, 12, 16):
+        if need4 <= c:
+            return (4, c)
+    return (4, 32)
 
 
 def outer_classes(n_outer: np.ndarray):
@@ -262,14 +264,14 @@ class SweepRunner:
                                       self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
                                       self.class_gmask[c], st.cuda_stream)
             nat.check(rc)
-            mark("k_fuse")
+            mark(f"k_fuse[{c}]")
             rc = self.lib.sk_map_outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
                                        self.segs.data_ptr(), self.fused.data_ptr(),
                                        self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
                                        0 if steps is None else steps.data_ptr() + 16 * a, mn,
                                        self.class_rows[c], st.cuda_stream)
             nat.check(rc)
-            mark("k_outer")
+            mark(f"k_outer[{c}]")
             if profile is None:
                 done = torch.cuda.Event()
                 done.record(side)
@@ -278,11 +280,13 @@ class SweepRunner:
             profile["events"] = evs
 
     @staticmethod
-    def kernel_ms(profile):
+    def kernel_ms(profile, per_class: bool = False):
         """Per-kernel milliseconds from a profiled solve (after synchronize)."""
         evs = profile["events"]
         out: dict[str, float] = {}
         for (_, e0), (tag, e1) in zip(evs, evs[1:]):
+            if not per_class:
+                tag = tag.split("[")[0]
             out[tag] = out.get(tag, 0.0) + e0.elapsed_time(e1)
         return out
 
