@@ -348,6 +348,8 @@ def run_reshard(world, rank, local, K=3, W=2, nccl_baseline=True):
     best = pull if pull["ms"] <= push["ms"] else push
     out = dict(best)
     out["modes_ms"] = {"pull": pull["ms"], "push": push["ms"]}
+    out["modes_progressive_ms"] = {"pull": pull["progressive"]["total_ms"],
+                                   "push": push["progressive"]["total_ms"]}
     if "nccl_grouped_sendrecv_ms" in pull:
         out["nccl_grouped_sendrecv_ms"] = pull["nccl_grouped_sendrecv_ms"]
         out["nccl_gbs_per_gpu"] = pull["nccl_gbs_per_gpu"]
@@ -387,6 +389,19 @@ def _reshard_once(world, rank, K, W, mode, nccl_baseline):
         e1.synchronize()
         times.append(allreduce_max(e0.elapsed_time(e1), world))
     bad = allreduce_sum(float(ex.verify()), world)
+    # progressive execution: per-round launches + stage-ready events
+    prog_total, stage_ready = [], {}
+    for _ in range(2):
+        dist.barrier()
+        torch.cuda.synchronize()
+        ready = ex.run_progressive()
+        end = torch.cuda.Event(enable_timing=True)
+        end.record()
+        end.synchronize()
+        prog_total.append(allreduce_max(ex.progress_begin.elapsed_time(end), world))
+        for st, ev in sorted(ready.items()):
+            stage_ready[st] = allreduce_max(ex.progress_begin.elapsed_time(ev), world)
+    bad += allreduce_sum(float(ex.verify()), world)
     t = min(times) / 1e3
     out = {
         "case": f"{name} bf16 {old}->{new}, KV batch 8 x seq 2048, {world} GPUs",
@@ -397,6 +412,8 @@ def _reshard_once(world, rank, K, W, mode, nccl_baseline):
         "byte_identical": bad == 0, "mismatched_words": int(bad),
         "local_bytes_rank0": ex.local_bytes, "transfers": len(plan.transfers()),
         "method": f"k_copy {mode} over CUDA-IPC peer mappings, 1 MiB chunks",
+        "progressive": {"total_ms": min(prog_total), "rounds": len(ex.round_ranges),
+                        "stage_ready_ms": {str(k): v for k, v in stage_ready.items()}},
     }
     if nccl_baseline:
         # grouped NCCL send/recv of the same transfers (the comparison path)

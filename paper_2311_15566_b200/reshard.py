@@ -107,10 +107,11 @@ def _find(entries, lo, hi):
     return None
 
 
-def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
+def plan_copies(plan, old_layout, new_required, model, seed: int = 1, with_rounds: bool = False):
     """Per destination GPU: the ordered byte-range copies that realise `plan`
     (the plan's transfers in plan order, then local reuse).
-    Returns (old slabs, new slabs, {dst gpu: [(src gpu, src_off, dst_off, bytes)]})."""
+    Returns (old slabs, new slabs, {dst gpu: [(src gpu, src_off, dst_off, bytes)]}); with
+    `with_rounds` also {dst gpu: [plan action index per copy]} (-1 = local reuse)."""
     rids = sorted({r for inv in list(old_layout.values()) + list(new_required.values())
                    for r, *_ in inv.cache_shards})
     rid_index = {r: i for i, r in enumerate(rids)}
@@ -118,7 +119,8 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
     new = {g: build_slab(inv, model, rid_index, seed, old.get(g)) for g, inv in new_required.items()}
     B, kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
     copies: dict = {g: [] for g in new}
-    for action in plan.actions:
+    rounds: dict = {g: [] for g in new}
+    for a_idx, action in enumerate(plan.actions):
         for t in action.transfers:
             if t.kind == "model":
                 src = _find(old[t.src].model.get(t.layer, ()), t.lo, t.hi)
@@ -138,6 +140,7 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
                 raise ValueError(f"transfer {t} targets a shard its destination already holds")
             copies[t.dst].append((t.src, src[-1][1] + _span(t.lo - src[0], unit),
                                   dst[-1][1] + _span(t.lo - dst[0], unit), n))
+            rounds[t.dst].append(a_idx)
     # local reuse: every needed piece the GPU already holds (the plan's "kept" bytes)
     for g, slab in new.items():
         have = old.get(g)
@@ -166,18 +169,23 @@ def plan_copies(plan, old_layout, new_required, model, seed: int = 1):
         # the copy kernel's CTAs take chunks in list order, so the local HBM
         # copies fill in behind the remote traffic instead of delaying it
         copies[g] = copies[g] + local
+        rounds[g] = rounds[g] + [-1] * len(local)
+    if with_rounds:
+        return old, new, copies, rounds
     return old, new, copies
 
 
-def issue_lists(copies: dict, owner: dict, mode: str = "pull") -> dict:
+def issue_lists(copies: dict, owner: dict, mode: str = "pull", rounds: dict | None = None) -> dict:
     """Which rank issues which copy: pull -> the destination GPU's rank, push ->
     the source GPU's rank; local (same-GPU) copies always by the owner.
-    Returns {rank: [(src, dst, src_off, dst_off, bytes)]} in plan order."""
+    Returns {rank: [(src, dst, src_off, dst_off, bytes)]} in plan order (with
+    `rounds`, each entry carries its plan action index as a 6th field)."""
     out: dict = {}
     for dst, lst in copies.items():
-        for src, soff, doff, n in lst:
+        for i, (src, soff, doff, n) in enumerate(lst):
             issuer = dst if (mode == "pull" or src == dst) else src
-            out.setdefault(owner[issuer], []).append((src, dst, soff, doff, n))
+            row = (src, dst, soff, doff, n) if rounds is None else (src, dst, soff, doff, n, rounds[dst][i])
+            out.setdefault(owner[issuer], []).append(row)
     return out
 
 
@@ -222,7 +230,9 @@ class ReshardExecutor:
             raise ValueError("mode must be 'pull' or 'push'")
         self.lib = nat.load()
         self.rank, self.world, self.mode = rank, world, mode
-        self.old, self.new, copies = plan_copies(plan, old_layout, new_required, model, seed)
+        self.old, self.new, copies, rounds = plan_copies(plan, old_layout, new_required, model, seed,
+                                                         with_rounds=True)
+        self.plan = plan
         self.mine = [g for g, r in owner.items() if r == rank]
         self.old_mem = {g: _Mem(self.old[g].bytes) for g in self.mine if g in self.old}
         self.new_mem = {g: _Mem(self.new[g].bytes) for g in self.mine if g in self.new}
@@ -253,10 +263,10 @@ class ReshardExecutor:
                     self.opened.append(p.value)
         self.peer_ptr = self.old_ptr
         dev = torch.device("cuda", torch.cuda.current_device())
-        rows = []
+        rows, rnd = [], []
         self.local_bytes = 0
         self.remote_bytes = 0
-        for src, dst, soff, doff, n in issue_lists(copies, owner, mode).get(rank, ()):
+        for src, dst, soff, doff, n, r in issue_lists(copies, owner, mode, rounds).get(rank, ()):
             if src == dst:
                 self.local_bytes += n
             else:
@@ -264,12 +274,29 @@ class ReshardExecutor:
             sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
             for c in range(0, n, CHUNK):
                 rows.append((sbase + soff + c, dbase + doff + c, min(CHUNK, n - c)))
-        arr = np.array(rows, dtype=np.uint64).reshape(-1, 3) if rows else np.zeros((0, 3), np.uint64)
-        cp = np.zeros(len(arr), dtype=nat.COPY)
-        if len(arr):
-            cp["src"], cp["dst"], cp["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
-        self.n_copies = len(cp)
-        self.d_copies = torch.from_numpy(cp.view(np.uint8)).to(dev) if len(cp) else None
+                rnd.append(r)
+
+        def to_dev(rs):
+            arr = np.array(rs, dtype=np.uint64).reshape(-1, 3) if rs else np.zeros((0, 3), np.uint64)
+            cp = np.zeros(len(arr), dtype=nat.COPY)
+            if len(arr):
+                cp["src"], cp["dst"], cp["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
+            return (torch.from_numpy(cp.view(np.uint8)).to(dev) if len(cp) else None), len(cp)
+
+        # one-launch order: NVLink transfers in plan order, local reuse last
+        self.d_copies, self.n_copies = to_dev(rows)
+        # progressive order: local reuse first, then round by round
+        order = sorted(range(len(rows)), key=lambda i: (rnd[i], i))
+        self.d_prog, _ = to_dev([rows[i] for i in order])
+        ro = [rnd[i] for i in order]
+        self.round_ranges = []   # (action index, begin, end) in the progressive array
+        i = 0
+        while i < len(ro):
+            j = i
+            while j < len(ro) and ro[j] == ro[i]:
+                j += 1
+            self.round_ranges.append((ro[i], i, j))
+            i = j
         self.d_fill = self._regions(self.old, self.old_mem, self.old_mem, dev)
         self.d_check = self._regions(self.new, self.new_mem, self.old_mem, dev)
         self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -297,6 +324,39 @@ class ReshardExecutor:
         if self.n_copies:
             nat.check(self.lib.sk_copy_batched(self.d_copies.data_ptr(), self.n_copies, n_ctas,
                                                torch.cuda.current_stream().cuda_stream))
+
+    def run_progressive(self, n_ctas: int = 0) -> dict:
+        """Round-by-round execution with a CUDA event per plan round, so a
+        stage can start serving as soon as the round its `start_stage` marker
+        follows has landed (PAPER.md:497's per-tensor readiness; the marker
+        placement is migration.py:352-371).  Returns {stage: event} recorded on
+        the current stream: this rank's copies for every round up to that
+        marker are complete when the event fires."""
+        st = torch.cuda.current_stream()
+        begin = torch.cuda.Event(enable_timing=True)
+        begin.record(st)
+        ptr = self.d_prog.data_ptr() if self.d_prog is not None else 0
+        ranges = {r: (b, e) for r, b, e in self.round_ranges}
+
+        def launch(r):
+            b, e = ranges[r]
+            nat.check(self.lib.sk_copy_batched(ptr + 24 * b, e - b, n_ctas, st.cuda_stream))
+
+        if -1 in ranges:
+            launch(-1)  # local reuse first (HBM only)
+        last = torch.cuda.Event(enable_timing=True)
+        last.record(st)
+        ready = {}
+        for idx, action in enumerate(self.plan.actions):
+            if action.kind == "start_stage":
+                ready[action.stage] = last
+                continue
+            if idx in ranges:
+                launch(idx)
+            last = torch.cuda.Event(enable_timing=True)
+            last.record(st)
+        self.progress_begin = begin
+        return ready
 
     def verify(self) -> int:
         """Mismatching 8-byte words in this rank's new slabs (0 = byte-identical)."""

@@ -4,6 +4,7 @@ multi-GPU run; peers are local pointers).  Resharded bytes must be identical
 to the regenerated pattern of the new layout."""
 
 import pytest
+import torch
 
 from paper_2311_15566_b200 import reshard
 
@@ -27,5 +28,23 @@ def test_reshard_byte_identical(old, new, mode):
         assert ex.verify() == 0
         bin_, bout = reshard.traffic(plan)
         assert ex.remote_bytes == sum(bin_.values())
+    finally:
+        ex.close()
+
+
+def test_progressive_rounds_and_stage_events():
+    plan, layout, need, model, refs = reshard.make_reshard_problem(SMALL, (1, 4, 2), (1, 2, 4),
+                                                                   batch=2, seq=64)
+    owner = {g: 0 for g in set(layout) | set(need)}
+    ex = reshard.ReshardExecutor(plan, layout, need, model, owner)
+    try:
+        ex.fill_old()
+        ready = ex.run_progressive()
+        torch.cuda.synchronize()
+        stages = {a.stage for a in plan.actions if a.kind == "start_stage"}
+        assert set(ready) == stages
+        times = {s: ex.progress_begin.elapsed_time(ev) for s, ev in ready.items()}
+        assert all(t >= 0 for t in times.values())
+        assert ex.verify() == 0
     finally:
         ex.close()
