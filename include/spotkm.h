@@ -276,6 +276,26 @@ typedef struct sk_timeline_input {
 
 int sk_plan_timeline(const sk_timeline_input* t, double* ends);
 
+/* Batched migration_cost (costmodel.py:231-260 over plan_timeline 189-228)
+ * for many candidate plans on the device, one thread per plan.  Per plan:
+ * actions [act_begin, act_end) (CSR act_ptr into the transfer arrays;
+ * act_stage = stage of a start_stage action, else -1), instances are
+ * plan-local ids with release floors at inst_base + i, scratch holds
+ * 2 * sum(n_inst) doubles and flags as many bytes. */
+typedef struct sk_tl_plan {
+  int32_t act_begin, act_end;
+  int32_t inst_base, n_inst;
+  double start, step; /* step = t_dec(config) / P, or 0 */
+  int32_t progressive, reserved;
+} sk_tl_plan; /* 40 bytes */
+
+int sk_migration_cost_batched(const sk_tl_plan* d_plans, int n_plans, const int32_t* d_act_ptr,
+                              const int32_t* d_act_stage, const int32_t* d_src_inst,
+                              const int32_t* d_dst_inst, const double* d_bytes,
+                              const uint8_t* d_has_release, const double* d_release,
+                              double* d_scratch, uint8_t* d_flags, double bandwidth,
+                              double latency, double* d_cost, void* stream);
+
 /* memopt_layer_order (migration.py:114-143) on per-layer traffic given as CSR
  * lists of (instance, bytes): incoming[l] and freed[l] for l in 0..L-1.
  * order receives L layer indices. */

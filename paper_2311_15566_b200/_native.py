@@ -33,6 +33,8 @@ SWEEP_DESC = np.dtype([("oD", "<i4"), ("oP", "<i4"), ("oM", "<i4"), ("G", "<i4")
                        ("kv", "<i8")], align=True)
 COPY = np.dtype([("src", "<u8"), ("dst", "<u8"), ("bytes", "<u8")], align=True)
 REGION = np.dtype([("ptr", "<u8"), ("bytes", "<u8"), ("key", "<u8"), ("base", "<u8")])
+TL_PLAN = np.dtype([("act_begin", "<i4"), ("act_end", "<i4"), ("inst_base", "<i4"), ("n_inst", "<i4"),
+                    ("start", "<f8"), ("step", "<f8"), ("progressive", "<i4"), ("reserved", "<i4")])
 assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize == 48 and COPY.itemsize == 24
 
 EXPORTS = (
@@ -42,7 +44,7 @@ EXPORTS = (
     "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
     "sk_ipc_open_handle", "sk_ipc_close_handle", "sk_fill_regions", "sk_verify_regions",
-    "sk_reshard_error",
+    "sk_reshard_error", "sk_migration_cost_batched",
 )
 
 
@@ -88,6 +90,8 @@ def load():
         "sk_fill_regions": ([vp, i32, vp], i32),
         "sk_verify_regions": ([vp, i32, vp, vp], i32),
         "sk_reshard_error": ([], ctypes.c_char_p),
+        "sk_migration_cost_batched": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_double,
+                                       ctypes.c_double, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -119,3 +119,101 @@ int sk_verify_regions(const sk_region* d_regions, int n, unsigned long long* d_b
 const char* sk_reshard_error(void) { return g_rerr; }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Batched T_mig estimator: plan_timeline + migration_cost (costmodel.py:189-260)
+// for many candidate plans at once, one thread per plan (each plan's timeline
+// is a sequential recurrence over its transfers).  Same double operations, in
+// the same order, as the host sk_plan_timeline / the reference.
+
+namespace {
+
+__global__ void k_migration_cost(const sk_tl_plan* __restrict__ plans, int n_plans,
+                                 const int32_t* __restrict__ act_ptr, const int32_t* __restrict__ act_stage,
+                                 const int32_t* __restrict__ src_inst, const int32_t* __restrict__ dst_inst,
+                                 const double* __restrict__ bytes, const uint8_t* __restrict__ has_release,
+                                 const double* __restrict__ release, double* __restrict__ scratch,
+                                 uint8_t* __restrict__ flags, double bandwidth, double latency,
+                                 double* __restrict__ cost) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_plans) return;
+  const sk_tl_plan p = plans[q];
+  double* out_free = scratch + 2 * (size_t)p.inst_base;
+  double* in_free = out_free + p.n_inst;
+  uint8_t* has_out = flags + 2 * (size_t)p.inst_base;
+  uint8_t* has_in = has_out + p.n_inst;
+  for (int i = 0; i < p.n_inst; ++i) {
+    has_out[i] = 0;
+    has_in[i] = 0;
+  }
+  const double start = p.start;
+  double prev = start;
+  // progressive bookkeeping: (stage, ready) of start_stage actions, sorted by stage
+  constexpr int kMaxStages = 64;
+  int st_stage[kMaxStages];
+  double st_ready[kMaxStages];
+  int n_st = 0;
+  for (int a = p.act_begin; a < p.act_end; ++a) {
+    double end = prev;
+    bool moved = false;
+    for (int k = act_ptr[a]; k < act_ptr[a + 1]; ++k) {
+      const int s = src_inst[k], d = dst_inst[k];
+      if (s == d) continue;
+      moved = true;
+      const int gs = p.inst_base + s, gd = p.inst_base + d;
+      const double so = has_out[s] ? out_free[s] : (has_release[gs] ? release[gs] : start);
+      const double di = has_in[d] ? in_free[d] : (has_release[gd] ? release[gd] : start);
+      const double begin = so > di ? so : di;
+      const double fin = begin + bytes[k] / bandwidth;
+      out_free[s] = fin;
+      has_out[s] = 1;
+      in_free[d] = fin;
+      has_in[d] = 1;
+      if (fin > end) end = fin;
+    }
+    if (moved) end += latency;
+    const double e = end > prev ? end : prev;
+    prev = e;
+    if (act_stage[a] >= 0 && n_st < kMaxStages) {
+      // insertion by stage keeps the stable sort of sorted(starts, key=stage)
+      int pos = n_st;
+      while (pos > 0 && st_stage[pos - 1] > act_stage[a]) {
+        st_stage[pos] = st_stage[pos - 1];
+        st_ready[pos] = st_ready[pos - 1];
+        --pos;
+      }
+      st_stage[pos] = act_stage[a];
+      st_ready[pos] = e;
+      ++n_st;
+    }
+  }
+  const double last = p.act_end > p.act_begin ? prev : start;
+  const double total = (last > start ? last : start) - start;
+  if (!p.progressive || n_st == 0) {
+    cost[q] = total;
+    return;
+  }
+  double stall = 0.0;
+  for (int o = 0; o < n_st; ++o) {
+    const double x = st_ready[o] - start - (double)o * p.step;
+    if (x > stall) stall = x;
+  }
+  cost[q] = stall > 0.0 ? stall : 0.0;
+}
+
+}  // namespace
+
+extern "C" int sk_migration_cost_batched(const sk_tl_plan* d_plans, int n_plans, const int32_t* d_act_ptr,
+                                         const int32_t* d_act_stage, const int32_t* d_src_inst,
+                                         const int32_t* d_dst_inst, const double* d_bytes,
+                                         const uint8_t* d_has_release, const double* d_release,
+                                         double* d_scratch, uint8_t* d_flags, double bandwidth,
+                                         double latency, double* d_cost, void* stream) {
+  if (n_plans <= 0) return SK_OK;
+  const int tpb = 128;
+  k_migration_cost<<<(n_plans + tpb - 1) / tpb, tpb, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_plans, n_plans, d_act_ptr, d_act_stage, d_src_inst, d_dst_inst, d_bytes, d_has_release,
+      d_release, d_scratch, d_flags, bandwidth, latency, d_cost);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SK_OK : rfail("k_migration_cost launch", e);
+}

@@ -413,3 +413,66 @@ def plan_from_dict(doc: dict, types=None):
     plan = T.MigrationPlan(actions=actions, u_max=doc.get("u_max"))
     plan.peak_usage = dict(doc.get("peak_usage", {}))
     return plan
+
+
+def migration_cost_many(plans, profile, configs=None, progressive=False, releases=None,
+                        starts=None) -> list:
+    """Batched `migration_cost` (costmodel.py:231-260) for many candidate plans
+    on the GPU, one thread per plan (`sk_migration_cost_batched`); the result
+    of each entry is bit-identical to `migration_cost` with the same
+    arguments.  `configs`, `releases`, `starts` are per-plan sequences (or None)."""
+    import torch
+
+    from .device import _device, _stream_ptr
+
+    Q = len(plans)
+    if Q == 0:
+        return []
+    configs = configs or [None] * Q
+    releases = releases or [None] * Q
+    starts = starts or [0.0] * Q
+    tl = np.zeros(Q, dtype=nat.TL_PLAN)
+    act_ptr, act_stage, src, dst, byt = [0], [], [], [], []
+    has_rel, rel = [], []
+    inst_base = 0
+    n_act = 0
+    for q, plan in enumerate(plans):
+        names: dict = {}
+        for action in plan.actions:
+            for tr in action.transfers:
+                src.append(names.setdefault(tr.src[0], len(names)))
+                dst.append(names.setdefault(tr.dst[0], len(names)))
+                byt.append(float(tr.bytes))
+            act_ptr.append(len(src))
+            act_stage.append(action.stage if action.kind == "start_stage" else -1)
+        r = releases[q] or {}
+        for name in r:
+            names.setdefault(name, len(names))
+        flags = [0] * len(names)
+        vals = [0.0] * len(names)
+        for name, t in r.items():
+            flags[names[name]] = 1
+            vals[names[name]] = float(t)
+        has_rel += flags
+        rel += vals
+        cfg = configs[q]
+        step = profile.decode_seconds(cfg) / cfg.pipeline_stages if cfg is not None else 0.0
+        tl[q] = (n_act, n_act + len(plan.actions), inst_base, len(names), float(starts[q]), step,
+                 1 if progressive else 0, 0)
+        n_act += len(plan.actions)
+        inst_base += len(names)
+    arrs = [np.array(act_ptr, np.int32), np.array(act_stage or [0], np.int32),
+            np.array(src or [0], np.int32), np.array(dst or [0], np.int32),
+            np.array(byt or [0.0], np.float64), np.array(has_rel or [0], np.uint8),
+            np.array(rel or [0.0], np.float64)]
+    dev = _device()
+    d = [torch.from_numpy(a).to(dev) for a in arrs]
+    d_tl = torch.from_numpy(tl.view(np.uint8)).to(dev)
+    scratch = torch.empty(max(2 * inst_base, 1), dtype=torch.float64, device=dev)
+    flags_d = torch.empty(max(2 * inst_base, 1), dtype=torch.uint8, device=dev)
+    cost = torch.empty(Q, dtype=torch.float64, device=dev)
+    rc = nat.load().sk_migration_cost_batched(
+        d_tl.data_ptr(), Q, *(x.data_ptr() for x in d), scratch.data_ptr(), flags_d.data_ptr(),
+        float(profile.bandwidth), float(profile.transfer_latency), cost.data_ptr(), _stream_ptr())
+    nat.check(rc)
+    return cost.cpu().tolist()
