@@ -30,9 +30,12 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     bad_total = 0
-    for old, new in CASES.get(world, CASES[2]):
+    cases = list(CASES.get(world, CASES[2]))
+    if world == 4:
+        cases += CASES[8]  # 8 GPU refs hosted 2 per rank: the driver's 8-GPU transitions
+    for old, new in cases:
         plan, layout, need, model, refs = reshard.make_reshard_problem(SMALL, old, new, 3, 64)
-        owner = {g: i for i, g in enumerate(refs)}
+        owner = {g: i * world // len(refs) for i, g in enumerate(refs)}
         for mode in ("pull", "push"):
             ex = reshard.ReshardExecutor(plan, layout, need, model, owner, rank, world, mode=mode)
             ex.fill_old()
