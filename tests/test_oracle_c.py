@@ -10,10 +10,13 @@ from oracle.sweep_inputs import plan_to_port
 from paper_2311_15566_b200 import sweep
 
 
-@pytest.mark.parametrize("n_pos,fused_sum", [(16, False), (32, False), (24, True)])
-def test_c_oracle_matches_port_on_sweep(n_pos, fused_sum):
+@pytest.mark.parametrize("n_pos,fused_sum,shapes,G", [
+    (16, False, sweep.GPT20B_SHAPES, 4), (32, False, sweep.GPT20B_SHAPES, 4),
+    (24, True, sweep.GPT20B_SHAPES, 4), (48, False, ((2, 3), (4, 3), (1, 6)), 3),
+    (24, True, ((2, 3), (2, 6), (3, 2)), 1)])
+def test_c_oracle_matches_port_on_sweep(n_pos, fused_sum, shapes, G):
     cport.build()
-    b = sweep.make_sweep(n_pos, 2, seed=n_pos, fused_sum=fused_sum)
+    b = sweep.make_sweep(n_pos, 2, seed=n_pos, fused_sum=fused_sum, shapes=shapes, G=G)
     assign, totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok, n_threads=4)
     for q in range(b.n_plans):
         inst, new, G, inh, reqs, fw = plan_to_port(b, q, sweep.GPT20B, n_requests=1 + q % 3)
