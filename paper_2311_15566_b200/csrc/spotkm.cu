@@ -436,7 +436,8 @@ __device__ __forceinline__ double lds_f64(unsigned a) {
 }
 
 __device__ __forceinline__ unsigned long long order_key(double x) {
-  const unsigned long long b = (unsigned long long)__double_as_longlong(x + 0.0);
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  if ((b << 1) == 0ull) b = 0ull;  // -0.0 ties with +0.0, as under '<'
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
@@ -538,12 +539,13 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   }
 
   // static column masks: valid = 1..n, real = 1..nB (beyond: zero padding)
-  unsigned long long valid = 0ull, real = 0ull;
+  static_assert(CPL <= 32, "32-bit column masks");
+  unsigned valid = 0u, real = 0u;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
     const int j = pt + T * k;
-    if (j >= 1 && j <= n) valid |= 1ull << k;
-    if (j >= 1 && j <= nB) real |= 1ull << k;
+    if (j >= 1 && j <= n) valid |= 1u << k;
+    if (j >= 1 && j <= nB) real |= 1u << k;
   }
   double v[CPL], minv[CPL];
   int wr[CPL];
@@ -560,10 +562,10 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   if (pt == 0) match[0] = 1;  // row 1 (ucol[0] = 0.0 already)
   plan_sync<W>();
 
-  long long nsteps = 0, nloads = 0;
+  int nsteps = 0, nloads = 0;
   int parity = 0;
   for (int i = 1; i <= n; ++i) {
-    unsigned long long used = (pt == 0) ? 1ull : 0ull;  // column 0
+    unsigned used = (pt == 0) ? 1u : 0u;  // column 0
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
     int j0 = 0;
@@ -571,41 +573,43 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       ++nsteps;
       const int i0 = match[j0];
       const double ui0 = ucol[j0];
-      const unsigned long long act = valid & ~used;
-      const unsigned long long ld = (i0 - 1) < nA ? (act & real) : 0ull;
+      const unsigned act = valid & ~used;
+      const unsigned ld = (i0 - 1) < nA ? (act & real) : 0u;
       const long long rowo = (long long)(i0 - 1) * nB - 1;
-      double cst[CPL];
+      // the row's weights w (cost = -w; padded entries are 0.0 -> cost -0.0)
+      double wx[CPL];
       if (CODED && coded) {
         // 32-bit shared-window addresses: one LDS.U8 + one LDS.64 per column
         const unsigned rowc = codes_s + (unsigned)((int)rowo + pt);
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
-          if ((ld >> k) & 1ull) x = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
-          cst[k] = -x;
+          if ((ld >> k) & 1u) x = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
+          wx[k] = x;
         }
       } else {
         const double* rowp = Fp + rowo + pt;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
-          if ((ld >> k) & 1ull) x = __ldg(rowp + T * k);
-          cst[k] = -x;
+          if ((ld >> k) & 1u) x = __ldg(rowp + T * k);
+          wx[k] = x;
         }
       }
-      nloads += __popcll(ld);
+      nloads += __popc(ld);
       double best = kInf;
       int bk = 0;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        const bool on = (act >> k) & 1ull;
-        const double cur = (cst[k] - ui0) - v[k];
+        const bool on = (act >> k) & 1u;
+        // (cost - u[i0]) - v[j] with cost = -w: the negation folds into the
+        // first DADD's operand modifiers (exact, same bits)
+        const double cur = (-wx[k] - ui0) - v[k];
         const bool imp = on && cur < minv[k];
         minv[k] = imp ? cur : minv[k];
         wr[k] = imp ? j0 : wr[k];
-        const double mk = on ? minv[k] : kInf;
-        const bool better = mk < best;
-        best = better ? mk : best;
+        const bool better = on && minv[k] < best;
+        best = better ? minv[k] : best;
         bk = better ? k : bk;
       }
       // argmin over (value, lowest j): order-preserving key, three redux.sync
@@ -642,21 +646,21 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       if (delta != 0.0) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
-          const bool u = (used >> k) & 1ull;
+          const bool u = (used >> k) & 1u;
           if (u) ucol[pt + T * k] += delta;
           v[k] = u ? v[k] - delta : v[k];
-          minv[k] = (!u && ((valid >> k) & 1ull)) ? minv[k] - delta : minv[k];
+          minv[k] = (!u && ((valid >> k) & 1u)) ? minv[k] - delta : minv[k];
         }
       }
       j0 = j1;
-      if (j0 % T == pt) used |= 1ull << (j0 / T);
+      if ((unsigned)j0 % (unsigned)T == (unsigned)pt) used |= 1u << ((unsigned)j0 / (unsigned)T);
       if (match[j0] == 0) break;
     }
     // publish predecessors, then walk the augmenting path (one thread), then
     // seed the next row
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
-      if (((used | valid) >> k) & 1ull) way[pt + T * k] = wr[k];
+      if (((used | valid) >> k) & 1u) way[pt + T * k] = wr[k];
     plan_sync<W>();
     if (pt == 0) {
       while (j0) {
@@ -698,7 +702,7 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   plan_sync<W>();
   if (A.steps) {
 #pragma unroll
-    for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);
+    for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);  // < 2^31 per plan
     if (pt == 0) A.steps[2 * q] = nsteps;
     if (W == 1) {
       if (lane == 0) A.steps[2 * q + 1] = nloads;
