@@ -299,7 +299,26 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
     return;
   }
   int pm[G];
-  hungarian_small<G>(w, pm);
+  // permutation-pattern block (exactly one positive weight per row and per
+  // column): the replayed KM matches every row to its positive column in a
+  // single Dijkstra step (the only negative reduced cost; no potential of a
+  // real column ever changes), so the answer is that permutation
+  bool is_perm = true;
+  unsigned colmask = 0;
+#pragma unroll
+  for (int k = 0; k < G; ++k) {
+    int cnt = 0, at = 0;
+#pragma unroll
+    for (int l = 0; l < G; ++l)
+      if (num[k][l] != 0) {
+        ++cnt;
+        at = l;
+      }
+    is_perm = is_perm && cnt == 1 && !((colmask >> at) & 1u);
+    colmask |= 1u << at;
+    pm[k] = at;
+  }
+  if (!is_perm) hungarian_small<G>(w, pm);
   double picked[G];
 #pragma unroll
   for (int k = 0; k < G; ++k) picked[k] = sel(w[k], pm[k]);

@@ -53,3 +53,19 @@ def test_tie_break_is_not_lexicographic(golden):
     W = [[0.0, 0.0, 2.0, 0.0], [1.0, 0.0, 1.0, 1.0], [0.0, 0.0, 2.0, 0.0], [0.0, 0.0, 0.0, 1.0]]
     assert port.hungarian_max(W) == [2, 0, 1, 3]
     _ = golden_w
+
+
+def test_permutation_pattern_blocks_match_their_permutation():
+    """Justifies k_fuse's fast path: on a block with exactly one positive
+    weight per row and column, the reference KM returns that permutation."""
+    import numpy as np
+
+    rng = np.random.default_rng(0)
+    for n in range(1, 9):
+        for _ in range(200):
+            sig = rng.permutation(n)
+            W = [[0.0] * n for _ in range(n)]
+            for k in range(n):
+                W[k][sig[k]] = float(rng.choice([rng.random() * 1e9, 1.0, 5e-324, 1e300,
+                                                 rng.integers(1, 10) / 3]))
+            assert port.hungarian_max(W) == list(sig)
