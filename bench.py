@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--model", default="gpt-20b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--all-sizes", action="store_true", help="also report 64..1024 positions")
+    ap.add_argument("--all-sizes", action=argparse.BooleanOptionalAction, default=True,
+                    help="also report 64..1024 positions (default on)")
     ap.add_argument("--no-reshard", action="store_true", help="skip the N>1 context reshard")
     return ap.parse_args()
 

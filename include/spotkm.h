@@ -113,19 +113,23 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
  *   d_total : per plan total_weight (accumulated in the reference order)
  *   max_na / max_nb = max fused rows / slots (R/g, C/g), max_rows = max R over the batch.
  *   group_mask: bit g set when some plan has group g (0 = any of 1..8).
+ *   fused_elems: elements of d_fused / d_perm in use (cleared first).
  */
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm,
                    int32_t* d_assign, double* d_total, int max_na, int max_nb,
-                   int max_rows, int group_mask, void* stream);
+                   int max_rows, int group_mask, int64_t fused_elems, void* stream);
 
 /* The two halves of sk_map_batched, for callers that time or pipeline them:
- * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  d_steps
+ * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  K2a only
+ * visits fused pairs that can be non-zero; [clear_begin, clear_begin +
+ * clear_count) of d_fused / d_perm is zeroed first (the encoding of an
+ * all-zero block), pass clear_count = 0 if the caller cleared it.  d_steps
  * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element
  * loads} (2 x int64) -- the algorithmic work of the outer KM. */
 int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                 const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na, int max_nb,
-                int group_mask, void* stream);
+                int group_mask, int64_t clear_begin, int64_t clear_count, void* stream);
 int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                  const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
                  int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,

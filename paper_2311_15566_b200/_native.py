@@ -75,8 +75,8 @@ def load():
         "sk_abi_version": ([], i32),
         "sk_last_error": ([], ctypes.c_char_p),
         "sk_build_weights": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
-        "sk_map_batched": ([vp, i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, vp], i32),
-        "sk_map_fuse": ([vp, i32, vp, vp, vp, vp, i32, i32, i32, vp], i32),
+        "sk_map_batched": ([vp, i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp], i32),
+        "sk_map_fuse": ([vp, i32, vp, vp, vp, vp, i32, i32, i32, i64, i64, vp], i32),
         "sk_map_outer": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], i32),
         "sk_km_dense": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),

@@ -279,9 +279,8 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
   const long long idx = p.f_off + (long long)a * nB + b;
   if (any == 0) {
     // all-zero block: max / builtin sum of zeros are 0.0 and the inner KM's
-    // answer is the (replayed) zero-matrix permutation
-    F[idx] = 0.0;
-    if (G > 1) perm_out[idx] = zero_perm;
+    // answer is the (replayed) zero-matrix permutation -- exactly what the
+    // pre-cleared buffers already encode (F = 0.0, perm stored XOR zero_perm)
     return;
   }
   // N / K: exact reciprocal multiply when K is a power of two (bit-identical
@@ -335,12 +334,22 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
 #pragma unroll
   for (int k = 0; k < G; ++k) packed |= (uint32_t)pm[k] << (4 * k);
   F[idx] = f;
-  perm_out[idx] = packed;
+  perm_out[idx] = packed ^ zero_perm;
 }
 
-// One thread per fused pair, pairs linear in (a, b) with b fastest: a warp's
-// lanes share their row group (broadcast segment loads).
+// One warp per fused GPU group a.  The fused matrix and perm buffers are
+// cleared beforehand (F = 0.0, perm = 0 meaning "zero-matrix permutation"),
+// so only pairs (a, b) that CAN be non-zero are visited: the warp reduces the
+// group's layer span [L0, L1) over its segments, and per new pipeline d only
+// the fused slots of stages overlapping that span are candidates (a
+// contiguous run of b).  Every other block is all-zero by construction.
 constexpr int kF_TPB = 128;
+constexpr int kF_WARPS = kF_TPB / 32;
+
+__device__ __forceinline__ int stage_of(int x, int L, int P) {
+  const int q = L / P, r = L % P;
+  return x < r * (q + 1) ? x / (q + 1) : r + (x - r * (q + 1)) / q;
+}
 
 template <int G>
 __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
@@ -352,10 +361,33 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   if (p.group != G) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
-  const long long pair = (long long)blockIdx.x * kF_TPB + threadIdx.x;
-  if (pair >= (long long)nA * nB) return;
-  const int a = (int)(pair / nB), b = (int)(pair % nB);
-  fuse_pair<G>(p, a, b, nB, col_of(p, b * G), row_ptr, segs, F, perm, zero_perm);
+  const int lane = threadIdx.x & 31;
+  const int a = blockIdx.x * kF_WARPS + (threadIdx.x >> 5);
+  if (a >= nA) return;  // warp-uniform
+  const int s_begin = row_ptr[p.row_base + a * G], s_end = row_ptr[p.row_base + a * G + G];
+  int lo = 0x7fffffff, hi = -1;
+  for (int s = s_begin + lane; s < s_end; s += 32) {
+    const sk_segment sg = segs[s];
+    if (sg.l1 > sg.l0 && sg.b > sg.a && sg.unit != 0) {
+      lo = min(lo, sg.l0);
+      hi = max(hi, sg.l1);
+    }
+  }
+  lo = __reduce_min_sync(kFull, lo);
+  hi = __reduce_max_sync(kFull, hi);
+  lo = max(lo, 0);
+  hi = min(hi, p.L);
+  if (lo >= hi) return;  // the whole row group is zero
+  const int p_lo = stage_of(lo, p.L, p.P), p_hi = stage_of(hi - 1, p.L, p.P);
+  const int span = ((p_hi + 1 - p_lo) * p.M) / G;  // fused slots per pipeline
+  const int per_d = (p.P * p.M) / G;
+  const int b0 = (p_lo * p.M) / G;
+  const int total = p.D * span;
+  for (int t = lane; t < total; t += 32) {
+    const int d = t / span;
+    const int b = d * per_d + b0 + (t - d * span);
+    fuse_pair<G>(p, a, b, nB, col_of(p, b * G), row_ptr, segs, F, perm, zero_perm);
+  }
 }
 
 // The inner KM's answer on an all-zero g x g block, replayed once on the host
@@ -372,13 +404,25 @@ uint32_t zero_block_perm() {
   return packed;
 }
 
+uint32_t zero_perm_of(int g) {
+  switch (g) {
+    case 2: { static const uint32_t z = zero_block_perm<2>(); return z; }
+    case 3: { static const uint32_t z = zero_block_perm<3>(); return z; }
+    case 4: { static const uint32_t z = zero_block_perm<4>(); return z; }
+    case 5: { static const uint32_t z = zero_block_perm<5>(); return z; }
+    case 6: { static const uint32_t z = zero_block_perm<6>(); return z; }
+    case 7: { static const uint32_t z = zero_block_perm<7>(); return z; }
+    case 8: { static const uint32_t z = zero_block_perm<8>(); return z; }
+    default: return 0u;
+  }
+}
+
 template <int G>
 int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
-  static const uint32_t zp = zero_block_perm<G>();
-  const long long bx = ((long long)max_na * max_nb + kF_TPB - 1) / kF_TPB;
-  dim3 grid((unsigned)bx, np);
-  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+  (void)max_nb;
+  dim3 grid((max_na + kF_WARPS - 1) / kF_WARPS, np);
+  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zero_perm_of(G));
   return cuda_check("k_fuse launch");
 }
 
@@ -435,6 +479,7 @@ struct OuterArgs {
   int32_t* assign;
   double* total;
   int64_t* steps;  // optional: {Dijkstra steps, cost loads} per plan (profiling)
+  uint32_t zero_perm[9];  // perm buffer stores (perm XOR zero_perm[g])
   size_t smem_per_warp;
   int max_n;
   int dbl_elems;
@@ -709,7 +754,8 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
     const int b = way[a];
     if (b < nB) {
       int col = b * g;
-      if (g > 1) col += (int)((A.perm[p.f_off + (long long)a * nB + b] >> (4 * k)) & 15u);
+      if (g > 1)
+        col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
       const double w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
       out[r] = col;
       wv[r] = w;
@@ -922,9 +968,15 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
 
 int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                 const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na, int max_nb,
-                int group_mask, void* stream) {
+                int group_mask, int64_t clear_begin, int64_t clear_count, void* stream) {
   if (n_plans < 0 || max_na < 0 || max_nb < 0) return set_err(SK_EINVAL, "negative sizes");
   if (n_plans == 0 || max_na == 0 || max_nb == 0) return SK_OK;
+  if (clear_count > 0) {
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(d_fused + clear_begin, 0, (size_t)clear_count * sizeof(double), cs) != cudaSuccess ||
+        cudaMemsetAsync(d_perm + clear_begin, 0, (size_t)clear_count * sizeof(uint32_t), cs) != cudaSuccess)
+      return cuda_check("clear fused buffers");
+  }
   if (((long long)max_na * max_nb + kF_TPB - 1) / kF_TPB > 0x7fffffffLL)
     return set_err(SK_EINVAL, "too many fused pairs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -951,16 +1003,17 @@ int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                  void* stream) {
   if (n_plans < 0 || max_n < 0 || max_rows < 0) return set_err(SK_EINVAL, "negative sizes");
   if (n_plans == 0) return SK_OK;
-  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, 0, max_n, 0};
+  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, {}, 0, max_n, 0};
+  for (int g = 0; g <= 8; ++g) A.zero_perm[g] = zero_perm_of(g);
   return outer_dispatch(A, max_rows, static_cast<cudaStream_t>(stream));
 }
 
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int32_t* d_assign,
                    double* d_total, int max_na, int max_nb, int max_rows, int group_mask,
-                   void* stream) {
+                   int64_t fused_elems, void* stream) {
   int rc = sk_map_fuse(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, max_na, max_nb,
-                       group_mask, stream);
+                       group_mask, 0, fused_elems, stream);
   if (rc) return rc;
   const int max_n = max_na > max_nb ? max_na : max_nb;
   return sk_map_outer(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, nullptr,
