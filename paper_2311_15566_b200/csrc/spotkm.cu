@@ -351,39 +351,45 @@ __device__ __forceinline__ int stage_of(int x, int L, int P) {
   return x < r * (q + 1) ? x / (q + 1) : r + (x - r * (q + 1)) / q;
 }
 
-template <int G>
+template <int G, int LPG>
 __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
                                                  const int32_t* __restrict__ row_ptr,
                                                  const sk_segment* __restrict__ segs,
                                                  double* __restrict__ F, uint32_t* __restrict__ perm,
                                                  uint32_t zero_perm) {
+  // LPG lanes per GPU group: small targets have few candidate slots per group
   const sk_plan p = plans[plan0 + blockIdx.y];
   if (p.group != G) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
-  const int lane = threadIdx.x & 31;
-  const int a = blockIdx.x * kF_WARPS + (threadIdx.x >> 5);
-  if (a >= nA) return;  // warp-uniform
-  const int s_begin = row_ptr[p.row_base + a * G], s_end = row_ptr[p.row_base + a * G + G];
+  const int lane = threadIdx.x & 31, sub = lane % LPG;
+  const int a = (blockIdx.x * kF_WARPS + (threadIdx.x >> 5)) * (32 / LPG) + lane / LPG;
+  const bool live = a < nA;
   int lo = 0x7fffffff, hi = -1;
-  for (int s = s_begin + lane; s < s_end; s += 32) {
-    const sk_segment sg = segs[s];
-    if (sg.l1 > sg.l0 && sg.b > sg.a && sg.unit != 0) {
-      lo = min(lo, sg.l0);
-      hi = max(hi, sg.l1);
+  if (live) {
+    const int s_begin = row_ptr[p.row_base + a * G], s_end = row_ptr[p.row_base + a * G + G];
+    for (int s = s_begin + sub; s < s_end; s += LPG) {
+      const sk_segment sg = segs[s];
+      if (sg.l1 > sg.l0 && sg.b > sg.a && sg.unit != 0) {
+        lo = min(lo, sg.l0);
+        hi = max(hi, sg.l1);
+      }
     }
   }
-  lo = __reduce_min_sync(kFull, lo);
-  hi = __reduce_max_sync(kFull, hi);
+#pragma unroll
+  for (int off = LPG / 2; off; off >>= 1) {
+    lo = min(lo, __shfl_xor_sync(kFull, lo, off));
+    hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+  }
   lo = max(lo, 0);
   hi = min(hi, p.L);
-  if (lo >= hi) return;  // the whole row group is zero
+  if (!live || lo >= hi) return;  // the whole row group is zero
   const int p_lo = stage_of(lo, p.L, p.P), p_hi = stage_of(hi - 1, p.L, p.P);
   const int span = ((p_hi + 1 - p_lo) * p.M) / G;  // fused slots per pipeline
   const int per_d = (p.P * p.M) / G;
   const int b0 = (p_lo * p.M) / G;
   const int total = p.D * span;
-  for (int t = lane; t < total; t += 32) {
+  for (int t = sub; t < total; t += LPG) {
     const int d = t / span;
     const int b = d * per_d + b0 + (t - d * span);
     fuse_pair<G>(p, a, b, nB, col_of(p, b * G), row_ptr, segs, F, perm, zero_perm);
@@ -420,9 +426,17 @@ uint32_t zero_perm_of(int g) {
 template <int G>
 int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
-  (void)max_nb;
-  dim3 grid((max_na + kF_WARPS - 1) / kF_WARPS, np);
-  k_fuse<G><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zero_perm_of(G));
+  // lanes per GPU group ~ the candidate slots a group typically has
+  const int lpg = max_nb <= 32 ? 8 : (max_nb <= 96 ? 16 : 32);
+  const int groups_per_block = kF_WARPS * (32 / lpg);
+  dim3 grid((max_na + groups_per_block - 1) / groups_per_block, np);
+  const uint32_t zp = zero_perm_of(G);
+  if (lpg == 8)
+    k_fuse<G, 8><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+  else if (lpg == 16)
+    k_fuse<G, 16><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+  else
+    k_fuse<G, 32><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
   return cuda_check("k_fuse launch");
 }
 
