@@ -134,12 +134,12 @@ class _Flat:
         self.K = K
         self.rids: dict = {}
         self.rid_names: list = []
+        rids = self.rids
 
         def rid(name):
-            r = self.rids.get(name)
+            r = rids.get(name)
             if r is None:
-                r = len(self.rid_names)
-                self.rids[name] = r
+                r = rids[name] = len(self.rid_names)
                 self.rid_names.append(name)
             return r
 
@@ -151,13 +151,20 @@ class _Flat:
             pos.append(-1 if p is None else ((p.pipeline - 1) * P + (p.stage - 1)) * M + (p.shard - 1))
         self.gpu_pos = np.array(pos, dtype=np.int32)
         mp, ms, cp, cs = [0], [], [0], []
+        scaled: dict = {}
+
+        def num(x):  # x * K as an integer, memoised by object identity (the
+            # endpoint Fractions are shared objects and stay alive for the call)
+            v = scaled.get(id(x))
+            if v is None:
+                v = x.numerator * (K // x.denominator)
+                scaled[id(x)] = v
+            return v
+
         for inv in invs:
-            for layer, lo, hi in inv.model_shards:
-                ms.append((layer, lo.numerator * (K // lo.denominator), hi.numerator * (K // hi.denominator)))
+            ms.extend((layer, num(lo), num(hi)) for layer, lo, hi in inv.model_shards)
             mp.append(len(ms))
-            for r_, layer, lo, hi, tok in inv.cache_shards:
-                cs.append((rid(r_), layer, lo.numerator * (K // lo.denominator),
-                           hi.numerator * (K // hi.denominator), tok))
+            cs.extend((rid(r_), layer, num(lo), num(hi), tok) for r_, layer, lo, hi, tok in inv.cache_shards)
             cp.append(len(cs))
         self.model_ptr = np.array(mp, dtype=np.int32)
         self.model_shards = np.array(ms, dtype=np.int64).reshape(-1, 3) if ms else np.zeros((0, 3), np.int64)
@@ -222,13 +229,19 @@ def _run(flat, u_max, derive_only, T):
 
 def _transfers(flat, tr, n, T):
     K, gpus, names = flat.K, flat.gpus, flat.rid_names
-    out = []
-    for t in tr[:n].tolist():
-        kind, layer, lo, hi, src, dst, b, rid, tok = t
-        out.append(T.Transfer(kind=_TRANSFER_KINDS[kind], layer=layer, lo=Fraction(lo, K),
-                              hi=Fraction(hi, K), src=gpus[src], dst=gpus[dst], bytes=b,
-                              request=None if rid < 0 else names[rid], tokens=tok))
-    return out
+    fracs: dict = {}
+
+    def frac(v):  # memoised Fraction(v, K): few distinct endpoints
+        f = fracs.get(v)
+        if f is None:
+            f = Fraction(v, K)
+            fracs[v] = f
+        return f
+
+    make, kinds = T.Transfer, _TRANSFER_KINDS
+    return [make(kind=kinds[kind], layer=layer, lo=frac(lo), hi=frac(hi), src=gpus[src],
+                 dst=gpus[dst], bytes=b, request=None if rid < 0 else names[rid], tokens=tok)
+            for kind, layer, lo, hi, src, dst, b, rid, tok in tr[:n].tolist()]
 
 
 # ---------------------------------------------------------------------------
