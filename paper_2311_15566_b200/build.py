@@ -11,6 +11,7 @@ import os
 import shutil
 import subprocess
 import sys
+import sysconfig
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -33,7 +34,24 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+HOSTPACK_SRC = PKG / "csrc" / "hostpack.cpp"
+HOSTPACK_OUT = PKG / f"_hostpack{sysconfig.get_config_var('EXT_SUFFIX')}"
+
+
+def build_hostpack(force: bool = False) -> Path:
+    """The CPython extension that flattens the caller's inventories (g++)."""
+    if not force and HOSTPACK_OUT.exists() and HOSTPACK_OUT.stat().st_mtime >= HOSTPACK_SRC.stat().st_mtime:
+        return HOSTPACK_OUT
+    cmd = ["g++", "-O2", "-std=c++17", "-shared", "-fPIC", f"-I{sysconfig.get_paths()['include']}",
+           "-o", str(HOSTPACK_OUT), str(HOSTPACK_SRC)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{res.stderr}")
+    return HOSTPACK_OUT
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    build_hostpack(force)
     OUT.parent.mkdir(parents=True, exist_ok=True)
     newest = max(p.stat().st_mtime for p in SRC + [ROOT / "include" / "spotkm.h"])
     if not force and OUT.exists() and OUT.stat().st_mtime >= newest:

@@ -1,0 +1,402 @@
+// hostpack.cpp -- CPython extension: flatten the caller's Python inventories
+// (tuples of Fractions, the reference's ContextInventory layout,
+// domain.py:175-220) into the integer arrays the C ABI consumes, without a
+// Python-level loop per shard.
+//
+//   common_denominator(invs, M)                 -> K
+//   pack_rows(invs, K, bpl, kv, need)           -> (row_ptr bytes, segments bytes)
+//       the segment encoding of pack.py (closed form of overlap_bytes,
+//       domain.py:299-320, on required_context_with_cache, mapping.py:155-169)
+//   flatten(invs, K, rid_index, rid_names)      -> (model_ptr, model_shards, cache_ptr, cache_shards)
+//       the planner input of include/spotkm.h sk_mig_input (rid strings interned
+//       into rid_index / rid_names)
+//
+// Exactness: all interval endpoints become integer numerators over K; the
+// numerator bound (< 2^53) is checked exactly with 128-bit integers.
+
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+
+#include <stdint.h>
+#include <string.h>
+
+#include <map>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+typedef __int128 i128;
+
+// y# with a NULL pointer builds None; empty buffers must stay bytes
+template <typename T>
+const char* bptr(const std::vector<T>& v) {
+  static const char empty = 0;
+  return v.empty() ? &empty : reinterpret_cast<const char*>(v.data());
+}
+
+struct Seg {
+  int32_t l0, l1, a, b, pipe, reserved;
+  int64_t unit;
+};
+static_assert(sizeof(Seg) == 32, "sk_segment layout");
+
+PyObject* g_num = nullptr;  // interned "numerator"
+PyObject* g_den = nullptr;  // interned "denominator"
+
+bool as_i64(PyObject* o, int64_t* out) {
+  int overflow = 0;
+  long long v = PyLong_AsLongLongAndOverflow(o, &overflow);
+  if (overflow || (v == -1 && PyErr_Occurred())) {
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_OverflowError, "integer out of int64 range");
+    return false;
+  }
+  *out = v;
+  return true;
+}
+
+// numerator / denominator of a Fraction (or int), memoised by object identity:
+// inventories share their endpoint objects
+struct FracCache {
+  std::unordered_map<PyObject*, std::pair<int64_t, int64_t>> m;
+  bool get(PyObject* x, int64_t* n, int64_t* d) {
+    auto it = m.find(x);
+    if (it != m.end()) {
+      *n = it->second.first;
+      *d = it->second.second;
+      return true;
+    }
+    PyObject* pn = PyObject_GetAttr(x, g_num);
+    if (!pn) return false;
+    PyObject* pd = PyObject_GetAttr(x, g_den);
+    if (!pd) {
+      Py_DECREF(pn);
+      return false;
+    }
+    const bool ok = as_i64(pn, n) && as_i64(pd, d);
+    Py_DECREF(pn);
+    Py_DECREF(pd);
+    if (!ok) return false;
+    m.emplace(x, std::make_pair(*n, *d));
+    return true;
+  }
+  bool scaled(PyObject* x, int64_t K, int64_t* v) {
+    int64_t n, d;
+    if (!get(x, &n, &d)) return false;
+    *v = n * (K / d);
+    return true;
+  }
+};
+
+// fetch attribute `name` of obj as a fast sequence (tuple/list)
+PyObject* seq_attr(PyObject* obj, const char* name) {
+  PyObject* a = PyObject_GetAttrString(obj, name);
+  if (!a) return nullptr;
+  PyObject* s = PySequence_Fast(a, "inventory shards must be a sequence");
+  Py_DECREF(a);
+  return s;
+}
+
+PyObject* py_common_denominator(PyObject*, PyObject* args) {
+  PyObject* invs;
+  long long M;
+  if (!PyArg_ParseTuple(args, "OL", &invs, &M)) return nullptr;
+  PyObject* seq = PySequence_Fast(invs, "inventories must be a sequence");
+  if (!seq) return nullptr;
+  FracCache fc;
+  int64_t K = M;
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(seq);
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* inv = PySequence_Fast_GET_ITEM(seq, i);
+    for (int part = 0; part < 2; ++part) {
+      PyObject* sh = seq_attr(inv, part == 0 ? "model_shards" : "cache_shards");
+      if (!sh) {
+        Py_DECREF(seq);
+        return nullptr;
+      }
+      const Py_ssize_t m = PySequence_Fast_GET_SIZE(sh);
+      const int lo_i = part == 0 ? 1 : 2;
+      for (Py_ssize_t k = 0; k < m; ++k) {
+        PyObject* t = PySequence_Fast_GET_ITEM(sh, k);
+        for (int e = 0; e < 2; ++e) {
+          PyObject* x = PySequence_GetItem(t, lo_i + e);
+          if (!x) {
+            Py_DECREF(sh);
+            Py_DECREF(seq);
+            return nullptr;
+          }
+          int64_t nu, de;
+          const bool ok = fc.get(x, &nu, &de);
+          Py_DECREF(x);
+          if (!ok) {
+            Py_DECREF(sh);
+            Py_DECREF(seq);
+            return nullptr;
+          }
+          K = std::lcm(K, de);
+          if (K > 0x7fffffffLL) {
+            Py_DECREF(sh);
+            Py_DECREF(seq);
+            PyErr_SetString(PyExc_ValueError, "common interval denominator exceeds 2^31-1");
+            return nullptr;
+          }
+        }
+      }
+      Py_DECREF(sh);
+    }
+  }
+  Py_DECREF(seq);
+  return PyLong_FromLongLong(K);
+}
+
+// need: dict rid -> list[(d_new, tokens)]
+typedef std::unordered_map<std::string, std::vector<std::pair<int32_t, int64_t>>> NeedMap;
+
+bool load_need(PyObject* need, NeedMap* out) {
+  if (need == Py_None) return true;
+  PyObject *key, *val;
+  Py_ssize_t pos = 0;
+  while (PyDict_Next(need, &pos, &key, &val)) {
+    Py_ssize_t len;
+    const char* s = PyUnicode_AsUTF8AndSize(key, &len);
+    if (!s) return false;
+    auto& v = (*out)[std::string(s, len)];
+    PyObject* seq = PySequence_Fast(val, "need entries must be a sequence");
+    if (!seq) return false;
+    for (Py_ssize_t i = 0; i < PySequence_Fast_GET_SIZE(seq); ++i) {
+      PyObject* pr = PySequence_Fast_GET_ITEM(seq, i);
+      PyObject* d = PySequence_GetItem(pr, 0);
+      PyObject* t = PySequence_GetItem(pr, 1);
+      int64_t dv = 0, tv = 0;
+      const bool ok = d && t && as_i64(d, &dv) && as_i64(t, &tv);
+      Py_XDECREF(d);
+      Py_XDECREF(t);
+      if (!ok) {
+        Py_DECREF(seq);
+        return false;
+      }
+      v.emplace_back((int32_t)dv, tv);
+    }
+    Py_DECREF(seq);
+  }
+  return true;
+}
+
+PyObject* py_pack_rows(PyObject*, PyObject* args) {
+  PyObject *invs, *need_obj;
+  long long K, bpl, kv;
+  if (!PyArg_ParseTuple(args, "OLLLO", &invs, &K, &bpl, &kv, &need_obj)) return nullptr;
+  NeedMap need;
+  if (!load_need(need_obj, &need)) return nullptr;
+  PyObject* seq = PySequence_Fast(invs, "inventories must be a sequence");
+  if (!seq) return nullptr;
+  FracCache fc;
+  const Py_ssize_t R = PySequence_Fast_GET_SIZE(seq);
+  std::vector<int32_t> row_ptr(R + 1, 0);
+  std::vector<Seg> segs;
+  const i128 limit = (i128)1 << 53;
+  for (Py_ssize_t r = 0; r < R; ++r) {
+    PyObject* inv = PySequence_Fast_GET_ITEM(seq, r);
+    // model: (a, b, layer) -> multiplicity
+    std::map<std::tuple<int64_t, int64_t, int64_t>, int64_t> model;
+    PyObject* ms = seq_attr(inv, "model_shards");
+    if (!ms) goto fail;
+    for (Py_ssize_t k = 0; k < PySequence_Fast_GET_SIZE(ms); ++k) {
+      PyObject* t = PySequence_Fast_GET_ITEM(ms, k);
+      PyObject *pl = PySequence_GetItem(t, 0), *plo = PySequence_GetItem(t, 1), *phi = PySequence_GetItem(t, 2);
+      int64_t layer = 0, a = 0, b = 0;
+      const bool ok = pl && plo && phi && as_i64(pl, &layer) && fc.scaled(plo, K, &a) && fc.scaled(phi, K, &b);
+      Py_XDECREF(pl);
+      Py_XDECREF(plo);
+      Py_XDECREF(phi);
+      if (!ok) {
+        Py_DECREF(ms);
+        goto fail;
+      }
+      model[std::make_tuple(a, b, layer)] += 1;
+    }
+    Py_DECREF(ms);
+    {
+      const size_t first = segs.size();
+      // runs of consecutive layers with equal (a, b, multiplicity)
+      for (auto& kvp : model) {
+        const int64_t a = std::get<0>(kvp.first), b = std::get<1>(kvp.first), layer = std::get<2>(kvp.first);
+        const int64_t unit = bpl * kvp.second;
+        if (segs.size() > first) {
+          Seg& s = segs.back();
+          if (s.pipe == 0 && s.a == a && s.b == b && s.unit == unit && s.l1 == layer) {
+            s.l1 = (int32_t)(layer + 1);
+            continue;
+          }
+        }
+        segs.push_back({(int32_t)layer, (int32_t)(layer + 1), (int32_t)a, (int32_t)b, 0, 0, unit});
+      }
+      if (!need.empty()) {
+        std::map<std::tuple<int64_t, int64_t, int32_t, int64_t>, int64_t> cache;
+        PyObject* cs = seq_attr(inv, "cache_shards");
+        if (!cs) goto fail;
+        for (Py_ssize_t k = 0; k < PySequence_Fast_GET_SIZE(cs); ++k) {
+          PyObject* t = PySequence_Fast_GET_ITEM(cs, k);
+          PyObject* prid = PySequence_GetItem(t, 0);
+          if (!prid) {
+            Py_DECREF(cs);
+            goto fail;
+          }
+          Py_ssize_t len;
+          const char* s = PyUnicode_AsUTF8AndSize(prid, &len);
+          if (!s) {
+            Py_DECREF(prid);
+            Py_DECREF(cs);
+            goto fail;
+          }
+          auto it = need.find(std::string(s, len));
+          Py_DECREF(prid);
+          if (it == need.end() || it->second.empty()) continue;
+          PyObject *pl = PySequence_GetItem(t, 1), *plo = PySequence_GetItem(t, 2),
+                   *phi = PySequence_GetItem(t, 3), *ptok = PySequence_GetItem(t, 4);
+          int64_t layer = 0, a = 0, b = 0, tok = 0;
+          const bool ok = pl && plo && phi && ptok && as_i64(pl, &layer) && fc.scaled(plo, K, &a) &&
+                          fc.scaled(phi, K, &b) && as_i64(ptok, &tok);
+          Py_XDECREF(pl);
+          Py_XDECREF(plo);
+          Py_XDECREF(phi);
+          Py_XDECREF(ptok);
+          if (!ok) {
+            Py_DECREF(cs);
+            goto fail;
+          }
+          for (auto& e : it->second) cache[std::make_tuple(a, b, e.first, layer)] += tok < e.second ? tok : e.second;
+        }
+        Py_DECREF(cs);
+        const size_t cfirst = segs.size();
+        for (auto& kvp : cache) {
+          const int64_t a = std::get<0>(kvp.first), b = std::get<1>(kvp.first), layer = std::get<3>(kvp.first);
+          const int32_t d = std::get<2>(kvp.first);
+          const int64_t tsum = kvp.second;
+          if (segs.size() > cfirst) {
+            Seg& s = segs.back();
+            if (s.pipe == d && s.a == a && s.b == b && s.unit == kv * tsum && s.l1 == layer && tsum != 0) {
+              s.l1 = (int32_t)(layer + 1);
+              continue;
+            }
+          }
+          if (tsum == 0) continue;
+          segs.push_back({(int32_t)layer, (int32_t)(layer + 1), (int32_t)a, (int32_t)b, d, 0, kv * tsum});
+        }
+      }
+      i128 bound = 0;
+      for (size_t i = first; i < segs.size(); ++i)
+        bound += (i128)(segs[i].l1 - segs[i].l0) * (segs[i].b - segs[i].a) * segs[i].unit;
+      if (bound >= limit) {
+        Py_DECREF(seq);
+        PyErr_SetString(PyExc_ValueError, "edge-weight numerator may exceed 2^53: outside the exact range");
+        return nullptr;
+      }
+    }
+    row_ptr[r + 1] = (int32_t)segs.size();
+  }
+  Py_DECREF(seq);
+  return Py_BuildValue("(y#y#)", bptr(row_ptr), (Py_ssize_t)(row_ptr.size() * 4), bptr(segs),
+                       (Py_ssize_t)(segs.size() * sizeof(Seg)));
+fail:
+  Py_DECREF(seq);
+  return nullptr;
+}
+
+PyObject* py_flatten(PyObject*, PyObject* args) {
+  PyObject *invs, *rid_index, *rid_names;
+  long long K;
+  if (!PyArg_ParseTuple(args, "OLO!O!", &invs, &K, &PyDict_Type, &rid_index, &PyList_Type, &rid_names))
+    return nullptr;
+  PyObject* seq = PySequence_Fast(invs, "inventories must be a sequence");
+  if (!seq) return nullptr;
+  FracCache fc;
+  const Py_ssize_t G = PySequence_Fast_GET_SIZE(seq);
+  std::vector<int32_t> mp(G + 1, 0), cp(G + 1, 0);
+  std::vector<int64_t> msh, csh;
+  for (Py_ssize_t g = 0; g < G; ++g) {
+    PyObject* inv = PySequence_Fast_GET_ITEM(seq, g);
+    PyObject* ms = seq_attr(inv, "model_shards");
+    if (!ms) goto fail;
+    for (Py_ssize_t k = 0; k < PySequence_Fast_GET_SIZE(ms); ++k) {
+      PyObject* t = PySequence_Fast_GET_ITEM(ms, k);
+      PyObject *pl = PySequence_GetItem(t, 0), *plo = PySequence_GetItem(t, 1), *phi = PySequence_GetItem(t, 2);
+      int64_t layer = 0, a = 0, b = 0;
+      const bool ok = pl && plo && phi && as_i64(pl, &layer) && fc.scaled(plo, K, &a) && fc.scaled(phi, K, &b);
+      Py_XDECREF(pl);
+      Py_XDECREF(plo);
+      Py_XDECREF(phi);
+      if (!ok) {
+        Py_DECREF(ms);
+        goto fail;
+      }
+      msh.push_back(layer);
+      msh.push_back(a);
+      msh.push_back(b);
+    }
+    Py_DECREF(ms);
+    mp[g + 1] = (int32_t)(msh.size() / 3);
+    PyObject* cs = seq_attr(inv, "cache_shards");
+    if (!cs) goto fail;
+    for (Py_ssize_t k = 0; k < PySequence_Fast_GET_SIZE(cs); ++k) {
+      PyObject* t = PySequence_Fast_GET_ITEM(cs, k);
+      PyObject *prid = PySequence_GetItem(t, 0), *pl = PySequence_GetItem(t, 1), *plo = PySequence_GetItem(t, 2),
+               *phi = PySequence_GetItem(t, 3), *ptok = PySequence_GetItem(t, 4);
+      int64_t layer = 0, a = 0, b = 0, tok = 0, rid = 0;
+      bool ok = prid && pl && plo && phi && ptok && as_i64(pl, &layer) && fc.scaled(plo, K, &a) &&
+                fc.scaled(phi, K, &b) && as_i64(ptok, &tok);
+      if (ok) {
+        PyObject* idx = PyDict_GetItemWithError(rid_index, prid);
+        if (idx) {
+          ok = as_i64(idx, &rid);
+        } else if (PyErr_Occurred()) {
+          ok = false;
+        } else {
+          rid = PyList_GET_SIZE(rid_names);
+          PyObject* pi = PyLong_FromLongLong(rid);
+          ok = pi && PyDict_SetItem(rid_index, prid, pi) == 0 && PyList_Append(rid_names, prid) == 0;
+          Py_XDECREF(pi);
+        }
+      }
+      Py_XDECREF(prid);
+      Py_XDECREF(pl);
+      Py_XDECREF(plo);
+      Py_XDECREF(phi);
+      Py_XDECREF(ptok);
+      if (!ok) {
+        Py_DECREF(cs);
+        goto fail;
+      }
+      csh.insert(csh.end(), {rid, layer, a, b, tok});
+    }
+    Py_DECREF(cs);
+    cp[g + 1] = (int32_t)(csh.size() / 5);
+  }
+  Py_DECREF(seq);
+  return Py_BuildValue("(y#y#y#y#)", bptr(mp), (Py_ssize_t)(mp.size() * 4), bptr(msh),
+                       (Py_ssize_t)(msh.size() * 8), bptr(cp), (Py_ssize_t)(cp.size() * 4), bptr(csh),
+                       (Py_ssize_t)(csh.size() * 8));
+fail:
+  Py_DECREF(seq);
+  return nullptr;
+}
+
+PyMethodDef kMethods[] = {
+    {"common_denominator", py_common_denominator, METH_VARARGS, "lcm of M and every interval denominator"},
+    {"pack_rows", py_pack_rows, METH_VARARGS, "inventories -> (row_ptr, segments) bytes"},
+    {"flatten", py_flatten, METH_VARARGS, "inventories -> planner arrays (bytes)"},
+    {nullptr, nullptr, 0, nullptr},
+};
+
+PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_hostpack", "native host-side packing", -1, kMethods};
+
+}  // namespace
+
+PyMODINIT_FUNC PyInit__hostpack(void) {
+  g_num = PyUnicode_InternFromString("numerator");
+  g_den = PyUnicode_InternFromString("denominator");
+  return PyModule_Create(&kModule);
+}

@@ -36,7 +36,25 @@ def _den(x) -> int:
     return x.denominator
 
 
+def _native():
+    try:
+        from . import _hostpack
+    except ImportError as e:  # built by paper_2311_15566_b200.build
+        raise RuntimeError("paper_2311_15566_b200._hostpack is not built "
+                           "(python -m paper_2311_15566_b200.build)") from e
+    return _hostpack
+
+
 def common_denominator(inventories, tensor_shards: int) -> int:
+    """lcm of M and every interval denominator (native)."""
+    try:
+        return _native().common_denominator(inventories, tensor_shards)
+    except ValueError as e:
+        raise PackError(str(e)) from None
+
+
+def py_common_denominator(inventories, tensor_shards: int) -> int:
+    """Pure-Python statement of common_denominator (cross-checked in tests)."""
     dens = {tensor_shards}
     for inv in inventories:
         for _, lo, hi in inv.model_shards:
@@ -125,7 +143,18 @@ def pack_row(inv, K: int, bpl: int, kv: int, need: dict):
 
 
 def pack_rows(inventories, K: int, bpl: int, kv: int, need: dict):
-    """-> (row_ptr int32[R+1], segments SEGMENT[S])."""
+    """-> (row_ptr int32[R+1], segments SEGMENT[S]) via the native packer
+    (csrc/hostpack.cpp), identical to py_pack_rows."""
+    try:
+        rp, sg = _native().pack_rows(inventories, K, bpl, kv, need)
+    except ValueError as e:
+        raise PackError(str(e)) from None
+    return np.frombuffer(rp, dtype=np.int32).copy(), np.frombuffer(sg, dtype=SEGMENT).copy()
+
+
+def py_pack_rows(inventories, K: int, bpl: int, kv: int, need: dict):
+    """Pure-Python statement of pack_rows: the readable spec the native packer
+    is tested against (tests/test_pack.py)."""
     rows = [pack_row(inv, K, bpl, kv, need) for inv in inventories]
     row_ptr = np.zeros(len(rows) + 1, dtype=np.int32)
     total = 0

@@ -15,7 +15,6 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass, field
 from fractions import Fraction
-from math import lcm
 
 import numpy as np
 
@@ -118,20 +117,11 @@ class _Flat:
         self.departing = np.array([1 if n in departing else 0 for n in self.insts], dtype=np.uint8)
         D, P, M = target.data_parallel, target.pipeline_stages, target.tensor_shards
         self.D, self.P, self.M = D, P, M
-        # common denominator
-        dens = {M}
+        # common denominator (native)
+        from .pack import common_denominator
+
         invs = [old_layout[g] for g in self.gpus]
-        for inv in invs:
-            for _, lo, hi in inv.model_shards:
-                dens.add(lo.denominator)
-                dens.add(hi.denominator)
-            for _, _, lo, hi, _ in inv.cache_shards:
-                dens.add(lo.denominator)
-                dens.add(hi.denominator)
-        K = 1
-        for d in dens:
-            K = lcm(K, d)
-        self.K = K
+        K = self.K = common_denominator(invs, M)
         self.rids: dict = {}
         self.rid_names: list = []
         rids = self.rids
@@ -150,26 +140,13 @@ class _Flat:
             p = mapping.assignment.get(g)
             pos.append(-1 if p is None else ((p.pipeline - 1) * P + (p.stage - 1)) * M + (p.shard - 1))
         self.gpu_pos = np.array(pos, dtype=np.int32)
-        mp, ms, cp, cs = [0], [], [0], []
-        scaled: dict = {}
+        from .pack import _native
 
-        def num(x):  # x * K as an integer, memoised by object identity (the
-            # endpoint Fractions are shared objects and stay alive for the call)
-            v = scaled.get(id(x))
-            if v is None:
-                v = x.numerator * (K // x.denominator)
-                scaled[id(x)] = v
-            return v
-
-        for inv in invs:
-            ms.extend((layer, num(lo), num(hi)) for layer, lo, hi in inv.model_shards)
-            mp.append(len(ms))
-            cs.extend((rid(r_), layer, num(lo), num(hi), tok) for r_, layer, lo, hi, tok in inv.cache_shards)
-            cp.append(len(cs))
-        self.model_ptr = np.array(mp, dtype=np.int32)
-        self.model_shards = np.array(ms, dtype=np.int64).reshape(-1, 3) if ms else np.zeros((0, 3), np.int64)
-        self.cache_ptr = np.array(cp, dtype=np.int32)
-        self.cache_shards = np.array(cs, dtype=np.int64).reshape(-1, 5) if cs else np.zeros((0, 5), np.int64)
+        mp, ms, cp, cs = _native().flatten(invs, K, self.rids, self.rid_names)
+        self.model_ptr = np.frombuffer(mp, dtype=np.int32).copy()
+        self.model_shards = np.frombuffer(ms, dtype=np.int64).reshape(-1, 3).copy()
+        self.cache_ptr = np.frombuffer(cp, dtype=np.int32).copy()
+        self.cache_shards = np.frombuffer(cs, dtype=np.int64).reshape(-1, 5).copy()
         self.inh_ptr = None
         self.inh_items = None
         if inherited_by_pipeline:

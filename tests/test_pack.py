@@ -56,6 +56,11 @@ def test_segments_reproduce_golden_weights(golden, name):
                                        model.kv_bytes_per_token_per_layer, need)
         W = eval_w(row_ptr, segs, K, cfg, model.num_layers)
         assert [[x.hex() for x in row] for row in W] == case["W"]
+        # the native packer (csrc/hostpack.cpp) equals the Python statement
+        assert K == pack.py_common_denominator(invs, cfg.tensor_shards)
+        rp2, sg2 = pack.py_pack_rows(invs, K, model.bytes_per_layer,
+                                     model.kv_bytes_per_token_per_layer, need)
+        assert rp2.tobytes() == row_ptr.tobytes() and sg2.tobytes() == segs.tobytes()
         checked += 1
     assert checked >= 10
 
@@ -69,4 +74,6 @@ def test_structured_row_is_one_model_and_one_cache_segment():
     inv = ContextInventory(inv_m, inv_c)
     need = {f"r{j}": [(1, 600 + j)] for j in range(4)}
     segs = pack.pack_row(inv, 8, 1000, 16, need)
+    rp, sg = pack.pack_rows([inv], 8, 1000, 16, need)
+    assert sg.tolist() == [(3, 9, 2, 4, 0, 0, 1000), (3, 9, 2, 4, 1, 0, 16 * (600 + 601 + 602 + 603))]
     assert segs == [(3, 9, 2, 4, 0, 1000), (3, 9, 2, 4, 1, 16 * (600 + 601 + 602 + 603))]
