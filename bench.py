@@ -545,7 +545,9 @@ def run_ours(args):
     if args.all_sizes:
         sizes = {}
         for n_pos in (64, 128, 256, 512, 1024):
-            sets = {64: 256, 128: 256, 256: 256, 512: 64, 1024: 32}[n_pos]
+            # enough plans per step to fill the GPU (big plans are long sequential
+            # chains: throughput comes from running many of them at once)
+            sets = 256
             b = sweep.make_sweep(n_pos, sets, seed=2000 + rank, model=geom, shapes=shapes)
             r = sweep.SweepRunner(b)
             k2 = max(2, K // 2)
