@@ -32,10 +32,6 @@ class PackError(ValueError):
     pass
 
 
-def _den(x) -> int:
-    return x.denominator
-
-
 def _native():
     try:
         from . import _hostpack
