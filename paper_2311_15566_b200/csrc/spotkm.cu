@@ -690,15 +690,26 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
         best = better ? minv[k] : best;
         bk = better ? k : bk;
       }
-      // argmin over (value, lowest j): order-preserving key, three redux.sync
       const unsigned bj = (best < kInf) ? (unsigned)(pt + T * bk) : 0xffffffffu;
+      unsigned jw;
+      double delta;
+      // fast path (~90% of steps on real plans): no negative slack and some
+      // zero slack -> the minimum is 0 and the reference's j1 is the lowest
+      // column whose slack is (+-)0; delta = 0 changes no potential
+      const unsigned any_neg = W == 1 ? __ballot_sync(kFull, best < 0.0) : 1u;
+      const unsigned any_zero = W == 1 ? __ballot_sync(kFull, best == 0.0) : 0u;
+      if (W == 1 && any_neg == 0u && any_zero != 0u) {
+        jw = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
+        delta = 0.0;
+      } else {
+      // argmin over (value, lowest j): order-preserving key, three redux.sync
       const unsigned long long key = order_key(best);
       const unsigned hi = __reduce_min_sync(kFull, (unsigned)(key >> 32));
       const bool c1 = (unsigned)(key >> 32) == hi;
       const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
       const bool c2 = c1 && (unsigned)key == lo;
-      unsigned jw = __reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
-      double delta = __shfl_sync(kFull, best, (jw % T) & 31);
+      jw = __reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
+      delta = __shfl_sync(kFull, best, (jw % T) & 31);
       if (W > 1) {
         Partial* pp = partial + parity * W;
         if (lane == 0) pp[pw] = {((unsigned long long)hi << 32) | lo, delta, jw, 0u};
@@ -716,6 +727,7 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
           }
         }
         parity ^= 1;
+      }
       }
       const int j1 = (int)jw;
       // a zero delta leaves every potential and slack numerically unchanged
