@@ -479,7 +479,7 @@ __host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int ma
                                                               int warps = 1) {
   size_t bytes = outer_base_bytes(max_n, max_rows);
   if (coded) bytes += (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + 15) & ~(size_t)15);
-  if (warps > 1) bytes += (size_t)2 * warps * 24;  // step partials (key, value, j)
+  if (warps > 1) bytes += (size_t)2 * warps * 24 + (size_t)4 * warps * 4;  // step partials
   return bytes;
 }
 
@@ -572,6 +572,7 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
   };
   Partial* partial = reinterpret_cast<Partial*>(
       base + (A.smem_per_warp - (size_t)2 * W * sizeof(Partial)));
+  unsigned* fastx = reinterpret_cast<unsigned*>(partial) - 4 * W;  // [2][W] x {neg, zero j}
   if (CODED) {
     for (int t = pt; t < kDictSlots; t += T) table[t] = kEmpty;
     plan_sync<W>();
@@ -696,10 +697,31 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
       // fast path (~90% of steps on real plans): no negative slack and some
       // zero slack -> the minimum is 0 and the reference's j1 is the lowest
       // column whose slack is (+-)0; delta = 0 changes no potential
-      const unsigned any_neg = W == 1 ? __ballot_sync(kFull, best < 0.0) : 1u;
-      const unsigned any_zero = W == 1 ? __ballot_sync(kFull, best == 0.0) : 0u;
-      if (W == 1 && any_neg == 0u && any_zero != 0u) {
-        jw = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
+      const unsigned any_neg = __ballot_sync(kFull, best < 0.0);
+      const unsigned any_zero = __ballot_sync(kFull, best == 0.0);
+      bool fast = any_neg == 0u && any_zero != 0u;
+      if (W == 1) {
+        if (fast) jw = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
+      } else {
+        // block-wide: combine the warps' (negative?, lowest zero column)
+        const unsigned zj = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
+        unsigned* fp = fastx + parity * 2 * W;
+        if (lane == 0) {
+          fp[2 * pw] = any_neg != 0u;
+          fp[2 * pw + 1] = zj;
+        }
+        __syncthreads();
+        bool gneg = false;
+        unsigned gz = 0xffffffffu;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          gneg = gneg || fp[2 * w] != 0u;
+          gz = min(gz, fp[2 * w + 1]);
+        }
+        fast = !gneg && gz != 0xffffffffu;
+        if (fast) jw = gz;
+      }
+      if (fast) {
         delta = 0.0;
       } else {
       // argmin over (value, lowest j): order-preserving key, three redux.sync
@@ -726,9 +748,9 @@ __global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
             delta = o.val;
           }
         }
-        parity ^= 1;
       }
       }
+      if (W > 1) parity ^= 1;
       const int j1 = (int)jw;
       // a zero delta leaves every potential and slack numerically unchanged
       // (at most flips the sign of a zero, which no comparison or later
