@@ -225,7 +225,7 @@ class ReshardExecutor:
     """
 
     def __init__(self, plan, old_layout, new_required, model, owner: dict, rank: int = 0,
-                 world: int = 1, seed: int = 1, group=None, mode: str = "pull"):
+                 world: int = 1, seed: int = 1, group=None, mode: str = "pull", chunk: int = CHUNK):
         if mode not in ("pull", "push"):
             raise ValueError("mode must be 'pull' or 'push'")
         self.lib = nat.load()
@@ -263,17 +263,22 @@ class ReshardExecutor:
                     self.opened.append(p.value)
         self.peer_ptr = self.old_ptr
         dev = torch.device("cuda", torch.cuda.current_device())
+        self._issued = issue_lists(copies, owner, mode, rounds).get(rank, ())
+        self._dev = dev
+        self.local_bytes = sum(n for src, dst, _, _, n, _ in self._issued if src == dst)
+        self.remote_bytes = sum(n for src, dst, _, _, n, _ in self._issued if src != dst)
+        self.set_chunk(chunk)
+        self.d_fill = self._regions(self.old, self.old_mem, self.old_mem, dev)
+        self.d_check = self._regions(self.new, self.new_mem, self.old_mem, dev)
+        self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def set_chunk(self, chunk: int = CHUNK):
+        """(Re)build the device copy lists with `chunk`-byte pieces."""
         rows, rnd = [], []
-        self.local_bytes = 0
-        self.remote_bytes = 0
-        for src, dst, soff, doff, n, r in issue_lists(copies, owner, mode, rounds).get(rank, ()):
-            if src == dst:
-                self.local_bytes += n
-            else:
-                self.remote_bytes += n
+        for src, dst, soff, doff, n, r in self._issued:
             sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
-            for c in range(0, n, CHUNK):
-                rows.append((sbase + soff + c, dbase + doff + c, min(CHUNK, n - c)))
+            for c in range(0, n, chunk):
+                rows.append((sbase + soff + c, dbase + doff + c, min(chunk, n - c)))
                 rnd.append(r)
 
         def to_dev(rs):
@@ -281,7 +286,7 @@ class ReshardExecutor:
             cp = np.zeros(len(arr), dtype=nat.COPY)
             if len(arr):
                 cp["src"], cp["dst"], cp["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
-            return (torch.from_numpy(cp.view(np.uint8)).to(dev) if len(cp) else None), len(cp)
+            return (torch.from_numpy(cp.view(np.uint8)).to(self._dev) if len(cp) else None), len(cp)
 
         # one-launch order: NVLink transfers in plan order, local reuse last
         self.d_copies, self.n_copies = to_dev(rows)
@@ -297,9 +302,6 @@ class ReshardExecutor:
                 j += 1
             self.round_ranges.append((ro[i], i, j))
             i = j
-        self.d_fill = self._regions(self.old, self.old_mem, self.old_mem, dev)
-        self.d_check = self._regions(self.new, self.new_mem, self.old_mem, dev)
-        self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
 
     @staticmethod
     def _regions(slabs, mems, old_mems, dev):
