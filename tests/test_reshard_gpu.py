@@ -48,3 +48,25 @@ def test_progressive_rounds_and_stage_events():
         assert ex.verify() == 0
     finally:
         ex.close()
+
+
+def test_executor_ingests_the_json_wire_plan():
+    """The paper ships plans as JSON over TCP; the executor
+    runs a plan that went through plan_to_dict -> json -> plan_from_dict."""
+    import json
+
+    from paper_2311_15566_b200 import planner
+
+    plan, layout, need, model, refs = reshard.make_reshard_problem(SMALL, (1, 2, 4), (2, 1, 4),
+                                                                   batch=2, seq=64)
+    wire = json.loads(json.dumps(planner.plan_to_dict(plan)))
+    back = planner.plan_from_dict(wire)
+    assert planner.plan_to_dict(back) == planner.plan_to_dict(plan)
+    owner = {g: 0 for g in set(layout) | set(need)}
+    ex = reshard.ReshardExecutor(back, layout, need, model, owner, mode="push")
+    try:
+        ex.fill_old()
+        ex.run()
+        assert ex.verify() == 0
+    finally:
+        ex.close()
