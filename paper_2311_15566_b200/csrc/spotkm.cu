@@ -533,7 +533,7 @@ __device__ __forceinline__ void plan_sync() {
 }
 
 template <int CPL, bool CODED, int W>
-__global__ void __launch_bounds__(kO_WARPS * 32) k_outer(const OuterArgs A) {
+__global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(const OuterArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int T = 32 * W;  // threads per plan
   const int pt = threadIdx.x % T, slot = threadIdx.x / T;
@@ -982,7 +982,10 @@ int outer_dispatch(const OuterArgs& A, int max_rows, cudaStream_t s) {
   if (need4 <= 8) return launch_outer<8, 4>(A, max_rows, s);
   if (need4 <= 12) return launch_outer<12, 4>(A, max_rows, s);
   if (need4 <= 16) return launch_outer<16, 4>(A, max_rows, s);
-  return set_err(SK_EINVAL, "outer KM size %d exceeds 2047", A.max_n);
+  const int need8 = (A.max_n + 1 + 255) / 256;  // columns per thread with 8 warps
+  if (need8 <= 12) return launch_outer<12, 8>(A, max_rows, s);
+  if (need8 <= 16) return launch_outer<16, 8>(A, max_rows, s);
+  return set_err(SK_EINVAL, "outer KM size %d exceeds 4095", A.max_n);
 }
 
 constexpr int kMaxGridY = 65535;

@@ -150,7 +150,8 @@ def cpl_bucket(n: int):
     for c in (3, 4, 5, 6, 8, 12, 16):
         if need4 <= c:
             return (4, c)
-    return (4, 32)
+    need8 = (n + 1 + 255) // 256
+    return (8, 12) if need8 <= 12 else (8, 16)
 
 
 def outer_classes(n_outer: np.ndarray):
