@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--positions", type=int, default=256)
-    ap.add_argument("--sets", type=int, default=256, help="preemption sets per config pair per step")
+    ap.add_argument("--sets", type=int, default=4096,
+                    help="preemption sets per config pair per step (BASELINE configs[2]: 4096)")
     ap.add_argument("--model", default="gpt-20b")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -262,6 +263,33 @@ def run_reference(args):
     }
     print(json.dumps(line))
     return 0
+
+
+# preemption sets per chunk for the all-sizes sweep (device scratch <= ~45 GB)
+SIZE_CHUNK_SETS = {64: 4096, 128: 4096, 256: 4096, 512: 2048, 1024: 1024}
+
+
+class Chunked:
+    """Consecutive SweepRunners (one sweep split into chunks) as one step."""
+
+    def __init__(self, runs):
+        self.runs = runs
+
+    def upload(self):
+        for r in self.runs:
+            r.upload()
+
+    def solve(self):
+        for r in self.runs:
+            r.solve()
+
+    def download(self):
+        for r in self.runs:
+            r.download()
+
+    def run(self):
+        for r in self.runs:
+            r.run()
 
 
 def measure_ours(runner, K, W, world, rank, local, flush, count_launches):
@@ -553,21 +581,32 @@ def run_ours(args):
     if world > 1 and not args.no_reshard:
         line["reshard"] = run_reshard(world, rank, local)
     if args.all_sizes:
+        del runner
         sizes = {}
         for n_pos in (64, 128, 256, 512, 1024):
-            # enough plans per step to fill the GPU (big plans are long sequential
-            # chains: throughput comes from running many of them at once)
-            sets = 256
-            b = sweep.make_sweep(n_pos, sets, seed=2000 + rank, model=geom, shapes=shapes)
-            r = sweep.SweepRunner(b)
-            k2 = max(2, K // 2)
-            d_ms, x_ms, _, _ = measure_ours(r, k2, 2, world, rank, local, flush, 0)
-            km, _ = kernel_breakdown(r, flush, 1)
-            sizes[str(n_pos)] = {"plans_per_step": b.n_plans,
-                                 "plans_per_s": b.n_plans * k2 / (d_ms / 1e3),
-                                 "e2e_plans_per_s": b.n_plans * k2 / (x_ms / 1e3),
+            # the full sweep (every config pair x args.sets preemption sets); at the
+            # large sizes it runs as consecutive chunks sharing one device scratch
+            chunk = min(args.sets, SIZE_CHUNK_SETS[n_pos])
+            bs = [sweep.make_sweep(n_pos, min(chunk, args.sets - c * chunk),
+                                   seed=2000 + 64 * rank + c, model=geom, shapes=shapes)
+                  for c in range(-(-args.sets // chunk))]
+            cap = (max(b.rows for b in bs), max(int(b.stats()["pairs"].sum()) for b in bs))
+            runs = []
+            for b in bs:
+                runs.append(sweep.SweepRunner(b, scratch=runs[0] if runs else None, reserve=cap))
+            chunked = Chunked(runs)
+            k2 = max(2, K // 2) if len(runs) == 1 else 2
+            d_ms, x_ms, _, _ = measure_ours(chunked, k2, 2, world, rank, local, flush, 0)
+            km = {}
+            for r in runs:
+                for k, v in kernel_breakdown(r, flush, 1)[0].items():
+                    km[k] = km.get(k, 0.0) + v
+            q = sum(r.b.n_plans for r in runs)
+            sizes[str(n_pos)] = {"plans_per_step": q, "chunks": len(runs),
+                                 "plans_per_s": q * k2 / (d_ms / 1e3),
+                                 "e2e_plans_per_s": q * k2 / (x_ms / 1e3),
                                  "kernels_ms_serialized": km}
-            del r
+            del runs, chunked
         line["sweep_sizes"] = sizes
     if rank == 0:
         print(json.dumps(line))

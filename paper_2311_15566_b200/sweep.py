@@ -178,7 +178,12 @@ class SweepRunner:
     KM), `download()` the D2H of assignments and totals.
     """
 
-    def __init__(self, batch: SweepBatch, device=None, stream=None):
+    def __init__(self, batch: SweepBatch, device=None, stream=None, scratch=None,
+                 reserve=(0, 0)):
+        """scratch: another SweepRunner whose device scratch (row_ptr, segments,
+        fused weights, permutations) this one reuses when large enough -- for
+        sweeps run as consecutive chunks on one stream; reserve: minimum
+        (rows, fused pairs) capacity to allocate for such sharing."""
         self.lib = nat.load()
         self.b = batch
         self.dev = torch.device(device or "cuda")
@@ -209,11 +214,19 @@ class SweepRunner:
         self.d_in = torch.empty(total, dtype=torch.uint8, device=self.dev)
         R = batch.rows
         Q = batch.n_plans
-        self.row_ptr = torch.empty(R + 1, dtype=torch.int32, device=self.dev)
-        self.segs = torch.empty(2 * R * 32, dtype=torch.uint8, device=self.dev)
-        pairs = int(st["pairs"].sum())
-        self.fused = torch.empty(max(pairs, 1), dtype=torch.float64, device=self.dev)
-        self.perm = torch.empty(max(pairs, 1), dtype=torch.int32, device=self.dev)
+        pairs = max(int(st["pairs"].sum()), 1, reserve[1])
+        Rcap = max(R, reserve[0])
+
+        def buf(name, n, dtype):
+            old = getattr(scratch, name, None)
+            if old is not None and old.numel() >= n:
+                return old
+            return torch.empty(n, dtype=dtype, device=self.dev)
+
+        self.row_ptr = buf("row_ptr", Rcap + 1, torch.int32)
+        self.segs = buf("segs", 2 * Rcap * 32, torch.uint8)
+        self.fused = buf("fused", pairs, torch.float64)
+        self.perm = buf("perm", pairs, torch.int32)
         self.out_bytes = _align(8 * Q + 4 * R)
         self.d_out = torch.empty(self.out_bytes, dtype=torch.uint8, device=self.dev)
         self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8, pin_memory=True)

@@ -53,3 +53,28 @@ def test_steps_counter_and_repeatability():
     n = b.stats()["n"]
     assert (s[:, 0] >= n).all()            # at least one Dijkstra step per row
     assert (s[:, 1] > 0).all()
+
+
+def test_chunks_sharing_scratch_match_c_oracle():
+    """A sweep run as consecutive chunks on one device scratch (bench.py's
+    all-sizes mode): every chunk still equals the oracle, run interleaved."""
+    import torch
+
+    bs = [sweep.make_sweep(256, 1 + c, seed=40 + c) for c in range(3)]
+    cap = (max(b.rows for b in bs), max(int(b.stats()["pairs"].sum()) for b in bs))
+    runs = []
+    for b in bs:
+        runs.append(sweep.SweepRunner(b, scratch=runs[0] if runs else None, reserve=cap))
+    assert all(r.fused is runs[0].fused and r.segs is runs[0].segs for r in runs)
+    for r in runs:
+        r.upload()
+    for r in runs:
+        r.solve()
+    for r in runs:
+        r.download()
+    torch.cuda.synchronize()
+    for r, b in zip(runs, bs):
+        assign, totals = r.results()
+        exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
+        assert np.array_equal(assign, exp_assign)
+        assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
