@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdint.h>
 #include <stdio.h>
 
@@ -246,12 +247,20 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
 // K2a: per fused pair (a, b): g x g block -> inner KM -> fused weight + perm
 
 
+// One fused pair's block result: fused weight and packed inner permutation.
+struct FusedBlock {
+  double f;
+  uint32_t packed;
+  bool nz;  // false: all-zero block (the pre-cleared buffers already hold it)
+};
+
+// Block of row group a x fused slot decoded by c0, counting the model
+// segments (pipe 0) and the cache segments of new pipeline `dsel` (0: model
+// only).  With dsel = c0.d this is exactly the reference's block.
 template <int G>
-__device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB, const Col c0,
-                                          const int32_t* __restrict__ row_ptr,
-                                          const sk_segment* __restrict__ segs,
-                                          double* __restrict__ F, uint32_t* __restrict__ perm_out,
-                                          uint32_t zero_perm) {
+__device__ __forceinline__ FusedBlock fuse_block(const sk_plan& p, int a, const Col c0, int dsel,
+                                                 const int32_t* __restrict__ row_ptr,
+                                                 const sk_segment* __restrict__ segs) {
   // the G columns of fused slot b share (pipeline, stage): c0 is their decode
   const int wdt = c0.i1 - c0.i0;
   long long num[G][G];
@@ -265,7 +274,7 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
     for (int s = s0; s < s1; ++s) {
       const sk_segment sg = segs[s];
       const int ol = min(sg.l1, c0.s1) - max(sg.l0, c0.s0);
-      if (ol <= 0 || (sg.pipe != 0 && sg.pipe != c0.d)) continue;
+      if (ol <= 0 || (sg.pipe != 0 && sg.pipe != dsel)) continue;
       const long long per = (long long)ol * sg.unit;
 #pragma unroll
       for (int l = 0; l < G; ++l) {
@@ -276,13 +285,14 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
 #pragma unroll
     for (int l = 0; l < G; ++l) any |= num[k][l];
   }
-  const long long idx = p.f_off + (long long)a * nB + b;
-  if (any == 0) {
-    // all-zero block: max / builtin sum of zeros are 0.0 and the inner KM's
-    // answer is the (replayed) zero-matrix permutation -- exactly what the
-    // pre-cleared buffers already encode (F = 0.0, perm stored XOR zero_perm)
-    return;
-  }
+  FusedBlock out;
+  out.f = 0.0;
+  out.packed = 0;
+  out.nz = any != 0;
+  // all-zero block: max / builtin sum of zeros are 0.0 and the inner KM's
+  // answer is the (replayed) zero-matrix permutation -- exactly what the
+  // pre-cleared buffers already encode (F = 0.0, perm stored XOR zero_perm)
+  if (!out.nz) return out;
   // N / K: exact reciprocal multiply when K is a power of two (bit-identical
   // to the correctly rounded division), else the IEEE division
   const bool pow2 = (p.K & (p.K - 1)) == 0;
@@ -294,8 +304,8 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
     for (int l = 0; l < G; ++l)
       w[k][l] = pow2 ? __ll2double_rn(num[k][l]) * inv : num_to_w(num[k][l], p.K);
   if (G == 1) {
-    F[idx] = w[0][0];  // max([w]) == sum([w]) == w for w >= 0
-    return;
+    out.f = w[0][0];  // max([w]) == sum([w]) == w for w >= 0
+    return out;
   }
   int pm[G];
   // permutation-pattern block (exactly one positive weight per row and per
@@ -333,18 +343,29 @@ __device__ __forceinline__ void fuse_pair(const sk_plan& p, int a, int b, int nB
   uint32_t packed = 0;
 #pragma unroll
   for (int k = 0; k < G; ++k) packed |= (uint32_t)pm[k] << (4 * k);
-  F[idx] = f;
-  perm_out[idx] = packed ^ zero_perm;
+  out.f = f;
+  out.packed = packed;
+  return out;
 }
 
-// One warp per fused GPU group a.  The fused matrix and perm buffers are
-// cleared beforehand (F = 0.0, perm = 0 meaning "zero-matrix permutation"),
-// so only pairs (a, b) that CAN be non-zero are visited: the warp reduces the
-// group's layer span [L0, L1) over its segments, and per new pipeline d only
-// the fused slots of stages overlapping that span are candidates (a
-// contiguous run of b).  Every other block is all-zero by construction.
+// One lane group (LPG lanes) per fused GPU group a.  The fused matrix and
+// perm buffers are cleared beforehand (F = 0.0, perm = 0 meaning "zero-matrix
+// permutation"), so only pairs (a, b) that CAN be non-zero are visited: the
+// lanes reduce the group's layer span [L0, L1) over its segments, and per new
+// pipeline d only the fused slots of stages overlapping that span are
+// candidates (a contiguous run of b).  Every other block is all-zero by
+// construction.
+//
+// A block depends on the new pipeline d only through the cache segments
+// tagged with d, so the lanes also reduce the set of pipelines the group's
+// cache segments name (a 128-bit mask).  The group's work items are then the
+// model-only block of each slot offset -- stored for every pipeline the mask
+// does not name -- and the full block of each (named pipeline, offset): the
+// same numbers give the same inner KM, so the reuse is exact, and a group
+// builds span * (1 + named pipelines) blocks instead of D * span.
 constexpr int kF_TPB = 128;
 constexpr int kF_WARPS = kF_TPB / 32;
+constexpr int kF_MAXD = 128;  // pipelines tracked by the cache-pipeline mask
 
 __device__ __forceinline__ int stage_of(int x, int L, int P) {
   const int q = L / P, r = L % P;
@@ -366,6 +387,8 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   const int a = (blockIdx.x * kF_WARPS + (threadIdx.x >> 5)) * (32 / LPG) + lane / LPG;
   const bool live = a < nA;
   int lo = 0x7fffffff, hi = -1;
+  unsigned long long pm0 = 0, pm1 = 0;  // cache pipelines 1..128 named by the group
+  bool pm_over = false;
   if (live) {
     const int s_begin = row_ptr[p.row_base + a * G], s_end = row_ptr[p.row_base + a * G + G];
     for (int s = s_begin + sub; s < s_end; s += LPG) {
@@ -373,6 +396,15 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
       if (sg.l1 > sg.l0 && sg.b > sg.a && sg.unit != 0) {
         lo = min(lo, sg.l0);
         hi = max(hi, sg.l1);
+        if (sg.pipe != 0) {
+          const int q = sg.pipe - 1;
+          if (q < 64)
+            pm0 |= 1ull << q;
+          else if (q < kF_MAXD)
+            pm1 |= 1ull << (q - 64);
+          else
+            pm_over = true;
+        }
       }
     }
   }
@@ -380,7 +412,10 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   for (int off = LPG / 2; off; off >>= 1) {
     lo = min(lo, __shfl_xor_sync(kFull, lo, off));
     hi = max(hi, __shfl_xor_sync(kFull, hi, off));
+    pm0 |= __shfl_xor_sync(kFull, pm0, off);
+    pm1 |= __shfl_xor_sync(kFull, pm1, off);
   }
+  pm_over = __any_sync(kFull, pm_over);
   lo = max(lo, 0);
   hi = min(hi, p.L);
   if (!live || lo >= hi) return;  // the whole row group is zero
@@ -388,11 +423,59 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   const int span = ((p_hi + 1 - p_lo) * p.M) / G;  // fused slots per pipeline
   const int per_d = (p.P * p.M) / G;
   const int b0 = (p_lo * p.M) / G;
-  const int total = p.D * span;
-  for (int t = sub; t < total; t += LPG) {
-    const int d = t / span;
-    const int b = d * per_d + b0 + (t - d * span);
-    fuse_pair<G>(p, a, b, nB, col_of(p, b * G), row_ptr, segs, F, perm, zero_perm);
+  if (pm_over) {
+    // more pipelines than the mask tracks: every candidate block in full
+    const int total = p.D * span;
+    for (int t = sub; t < total; t += LPG) {
+      const int d = t / span;
+      const int b = d * per_d + b0 + (t - d * span);
+      const Col c0 = col_of(p, b * G);
+      const FusedBlock r = fuse_block<G>(p, a, c0, c0.d, row_ptr, segs);
+      if (r.nz) {
+        const long long idx = p.f_off + (long long)a * nB + b;
+        F[idx] = r.f;
+        perm[idx] = r.packed ^ zero_perm;
+      }
+    }
+    return;
+  }
+  // work items: the model-only block of every slot offset (stored for every
+  // pipeline the group's cache does not name), then the full block of every
+  // (named pipeline, offset)
+  const int nbits = __popcll(pm0) + __popcll(pm1);
+  const int n_items = span * (1 + nbits);
+  const long long row0 = p.f_off + (long long)a * nB;
+  for (int it = sub; it < n_items; it += LPG) {
+    int o = it, dq = -1;  // dq: 0-based named pipeline, -1 = model only
+    if (it >= span) {
+      const int k = (it - span) / span;
+      o = it - span - k * span;
+      // k-th set bit of the mask
+      unsigned long long m = pm0;
+      int base = 0, kk = k;
+      if (kk >= __popcll(pm0)) {
+        kk -= __popcll(pm0);
+        m = pm1;
+        base = 64;
+      }
+      for (int z = 0; z < kk; ++z) m &= m - 1;
+      dq = base + __ffsll(m) - 1;
+    }
+    const int bq = (dq < 0 ? 0 : dq) * per_d + b0 + o;
+    const FusedBlock r = fuse_block<G>(p, a, col_of(p, bq * G), dq + 1, row_ptr, segs);
+    if (!r.nz) continue;
+    const uint32_t pk = r.packed ^ zero_perm;
+    if (dq >= 0) {
+      F[row0 + bq] = r.f;
+      perm[row0 + bq] = pk;
+    } else {
+      for (int d = 0; d < p.D; ++d) {
+        if ((d < 64 ? pm0 >> d : pm1 >> (d - 64)) & 1ull) continue;
+        const int b = d * per_d + b0 + o;
+        F[row0 + b] = r.f;
+        perm[row0 + b] = pk;
+      }
+    }
   }
 }
 
@@ -427,11 +510,20 @@ template <int G>
 int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, const int32_t* row_ptr,
                 const sk_segment* segs, double* F, uint32_t* perm, cudaStream_t s) {
   // lanes per GPU group ~ the candidate slots a group typically has
-  const int lpg = max_nb <= 32 ? 8 : (max_nb <= 96 ? 16 : 32);
+  // a group has ~span * (1 + cache pipelines) blocks to build, whatever nB
+  static const int env_lpg = [] {
+    const char* e = getenv("SK_FUSE_LPG");
+    return e ? atoi(e) : 0;
+  }();
+  const int lpg = env_lpg ? env_lpg : 4;
   const int groups_per_block = kF_WARPS * (32 / lpg);
   dim3 grid((max_na + groups_per_block - 1) / groups_per_block, np);
   const uint32_t zp = zero_perm_of(G);
-  if (lpg == 8)
+  if (lpg == 2)
+    k_fuse<G, 2><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+  else if (lpg == 4)
+    k_fuse<G, 4><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+  else if (lpg == 8)
     k_fuse<G, 8><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
   else if (lpg == 16)
     k_fuse<G, 16><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
