@@ -555,8 +555,7 @@ def run_ours(args):
         "roofline": roofline,
         "kernels_ms_per_step_serialized": {k: v["ms"] for k, v in kernels.items()},
         "outer_km": {"dijkstra_steps_per_plan": float(st[:, 0].mean()),
-                     "steps_per_s": float(st[:, 0].sum()) / (kernels["k_outer"]["ms"] / 1e3),
-                     "cost_loads_per_plan": float(st[:, 1].mean())},
+                     "steps_per_s": float(st[:, 0].sum()) / (kernels["k_outer"]["ms"] / 1e3)},
         "pipeline_roofline": {"bytes_per_plan_16RC": survey_bytes / batch.n_plans,
                               "ceiling_plans_per_s": hbm * 1e9 * batch.n_plans / survey_bytes,
                               "frac": value / world / (hbm * 1e9 * batch.n_plans / survey_bytes)},

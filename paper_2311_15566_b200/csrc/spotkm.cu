@@ -552,8 +552,10 @@ int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, 
 
 constexpr int kO_WARPS = 4;
 
-__host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows) {
-  return max_n + 1 > max_rows ? max_n + 1 : max_rows;
+// doubles at the head of a plan's shared region: ucol (n + 1), and in the
+// epilogue the per-row weights (rows) unless those go to the dictionary area
+__host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows, bool wv_in_dict) {
+  return wv_in_dict || max_n + 1 > max_rows ? max_n + 1 : max_rows;
 }
 // Dictionary coding of the fused matrix: real fused weights take few distinct
 // values (2-5 distinct per row), so the warp packs its plan's
@@ -563,14 +565,24 @@ __host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows)
 constexpr int kDictSlots = 256;
 constexpr unsigned long long kEmpty = ~0ull;  // a NaN pattern: never a weight
 
-__host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int max_rows) {
-  size_t bytes = (size_t)outer_dbl_elems(max_n, max_rows) * 8 + (size_t)(max_n + 1) * 4 * 2;
+// match / way are int16 (n <= 4095)
+__host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int dbl_elems) {
+  size_t bytes = (size_t)dbl_elems * 8 + (size_t)(max_n + 1) * 2 * 2;
   return (bytes + 15) & ~(size_t)15;
 }
+// codes: the zero-padded n x n matrix (row stride n) + slack for the
+// unpredicated per-step row reads (slot k of thread t reads column t + T k)
+__host__ __device__ __forceinline__ size_t outer_dict_bytes(int max_n, int slack) {
+  return (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + slack + 15) & ~(size_t)15);
+}
+__host__ __device__ __forceinline__ bool outer_wv_in_dict(int max_n, int max_rows) {
+  return (size_t)max_rows * 8 <= outer_dict_bytes(max_n, 0);
+}
 __host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, bool coded,
-                                                              int warps = 1) {
-  size_t bytes = outer_base_bytes(max_n, max_rows);
-  if (coded) bytes += (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + 15) & ~(size_t)15);
+                                                              int warps, int cpl) {
+  size_t bytes =
+      outer_base_bytes(max_n, outer_dbl_elems(max_n, max_rows, coded && outer_wv_in_dict(max_n, max_rows)));
+  if (coded) bytes += outer_dict_bytes(max_n, 32 * warps * cpl);
   if (warps > 1) bytes += (size_t)2 * warps * 24 + (size_t)4 * warps * 4;  // step partials
   return bytes;
 }
@@ -589,6 +601,7 @@ struct OuterArgs {
   size_t smem_per_warp;
   int max_n;
   int dbl_elems;
+  int wv_in_dict;  // CODED: epilogue row weights live in the dictionary area
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -640,12 +653,12 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   const int n = nA > nB ? nA : nB;
   const int n1 = A.max_n + 1;
 
-  // per-plan layout: [double ucol / wv: dbl_elems] [int match: n1] [int way: n1]
-  //                  [CODED: u64 table[256] | u8 codes[max_n^2]] ; W > 1 partials after
+  // per-plan layout: [double ucol (/ wv): dbl_elems] [i16 match: n1] [i16 way: n1]
+  //                  [CODED: u64 table[256] | u8 codes[max_n^2] (/ wv)] ; W > 1 partials after
   unsigned char* base = smem + (size_t)slot * A.smem_per_warp;
   double* ucol = reinterpret_cast<double*>(base);
-  int* match = reinterpret_cast<int*>(base + (size_t)A.dbl_elems * 8);
-  int* way = match + n1;
+  short* match = reinterpret_cast<short*>(base + (size_t)A.dbl_elems * 8);
+  short* way = match + n1;
 
   const double* Fp = A.F + p.f_off;
   // dictionary-code the fused matrix into shared memory (CODED variant).
@@ -666,17 +679,27 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       base + (A.smem_per_warp - (size_t)2 * W * sizeof(Partial)));
   unsigned* fastx = reinterpret_cast<unsigned*>(partial) - 4 * W;  // [2][W] x {neg, zero j}
   if (CODED) {
-    for (int t = pt; t < kDictSlots; t += T) table[t] = kEmpty;
+    // slot 0 holds +0.0 (its own hash slot), the code of the zero padding
+    for (int t = pt; t < kDictSlots; t += T) table[t] = t == 0 ? 0ull : kEmpty;
     plan_sync<W>();
     bool fail = false;
-    const int cnt = nA * nB;
     constexpr int U = 8;  // independent loads in flight per thread
+    const int cnt = n * n;  // < 2^24: exact in float
+    const float inv_n = 1.0f / (float)n;
     for (int e0 = 0; e0 < cnt; e0 += T * U) {
       unsigned long long bits[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        // branch-free (r, c) = divmod(e, n) and an always-valid address, so
+        // the U loads stay in flight together
         const int e = e0 + u * T + pt;
-        bits[u] = e < cnt ? (unsigned long long)__double_as_longlong(__ldg(Fp + e)) : kEmpty;
+        int r = (int)((float)e * inv_n);
+        int c = e - r * n;
+        r = c < 0 ? r - 1 : (c >= n ? r + 1 : r);
+        c = c < 0 ? c + n : (c >= n ? c - n : c);
+        const bool in = e < cnt && r < nA && c < nB;
+        const unsigned long long x = (unsigned long long)__double_as_longlong(__ldg(Fp + (in ? r * nB + c : 0)));
+        bits[u] = in ? x : (e < cnt ? 0ull : kEmpty);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -698,7 +721,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
           }
         }
         h = __shfl_sync(kFull, h, leader);
-        if (e < cnt) codes[e] = (unsigned char)h;
+        if (bits[u] != kEmpty) codes[e] = (unsigned char)h;
       }
     }
     if (W == 1) {
@@ -733,7 +756,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   if (pt == 0) match[0] = 1;  // row 1 (ucol[0] = 0.0 already)
   plan_sync<W>();
 
-  int nsteps = 0, nloads = 0;
+  int nsteps = 0, nloads = 0;  // nloads: uncoded path only
   int parity = 0;
   for (int i = 1; i <= n; ++i) {
     unsigned used = (pt == 0) ? 1u : 0u;  // column 0
@@ -745,29 +768,26 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       const int i0 = match[j0];
       const double ui0 = ucol[j0];
       const unsigned act = valid & ~used;
-      const unsigned ld = (i0 - 1) < nA ? (act & real) : 0u;
-      const long long rowo = (long long)(i0 - 1) * nB - 1;
       // the row's weights w (cost = -w; padded entries are 0.0 -> cost -0.0)
       double wx[CPL];
       if (CODED && coded) {
-        // 32-bit shared-window addresses: one LDS.U8 + one LDS.64 per column
-        const unsigned rowc = codes_s + (unsigned)((int)rowo + pt);
+        // the padded n x n code matrix: unpredicated reads, one LDS.U8 + one
+        // LDS.64 per column (32-bit shared-window addresses); reads for
+        // columns outside 1..n land in the slack and are never used
+        const unsigned rowc = codes_s + (unsigned)((i0 - 1) * n + pt - 1);
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) {
-          double x = 0.0;
-          if ((ld >> k) & 1u) x = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
-          wx[k] = x;
-        }
+        for (int k = 0; k < CPL; ++k) wx[k] = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
       } else {
-        const double* rowp = Fp + rowo + pt;
+        const unsigned ld = (i0 - 1) < nA ? (act & real) : 0u;
+        const double* rowp = Fp + ((i0 - 1) * nB - 1) + pt;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
           if ((ld >> k) & 1u) x = __ldg(rowp + T * k);
           wx[k] = x;
         }
+        nloads += __popc(ld);
       }
-      nloads += __popc(ld);
       double best = kInf;
       int bk = 0;
 #pragma unroll
@@ -864,7 +884,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
     // seed the next row
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
-      if (((used | valid) >> k) & 1u) way[pt + T * k] = wr[k];
+      if (((used | valid) >> k) & 1u) way[pt + T * k] = (short)wr[k];
     plan_sync<W>();
     if (pt == 0) {
       while (j0) {
@@ -873,7 +893,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         ucol[j0] = ucol[j1];
         j0 = j1;
       }
-      match[0] = i + 1;
+      match[0] = (short)(i + 1);
       ucol[0] = 0.0;
     }
     plan_sync<W>();
@@ -882,10 +902,10 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   // row_to_col for real fused rows -> way[] (free now)
   for (int j = pt + 1; j <= n; j += T) {
     const int r = match[j];
-    if (r >= 1 && r <= nA) way[r - 1] = j - 1;
+    if (r >= 1 && r <= nA) way[r - 1] = (short)(j - 1);
   }
   plan_sync<W>();
-  double* wv = ucol;
+  double* wv = (CODED && A.wv_in_dict) ? reinterpret_cast<double*>(table) : ucol;
   int32_t* out = A.assign + p.out_off;
   const int32_t* __restrict__ row_ptr = A.row_ptr;
   const sk_segment* __restrict__ segs = A.segs;
@@ -1019,23 +1039,43 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
   }
 }
 
+// plans per block (W == 1) maximising the plans resident per SM under the
+// shared-memory (incl. the 1 KB per-block reserve), thread and block limits
+int best_per_block(size_t plan_smem, int W, size_t cap) {
+  constexpr size_t kSmemSM = 228 * 1024, kReserve = 1024;
+  int best = 0, best_res = 0;
+  for (int pb = 1; pb <= (W == 1 ? kO_WARPS : 1); ++pb) {
+    const size_t blk = plan_smem * pb;
+    if (blk > cap) break;
+    int nb = (int)(kSmemSM / (blk + kReserve));
+    nb = nb < 2048 / (32 * W * pb) ? nb : 2048 / (32 * W * pb);
+    nb = nb < 32 ? nb : 32;
+    if (nb * pb >= best_res && nb > 0) {
+      best_res = nb * pb;
+      best = pb;
+    }
+  }
+  return best;
+}
+
 template <int CPL, int W>
 int launch_outer(OuterArgs A, int max_rows, cudaStream_t s) {
-  A.dbl_elems = outer_dbl_elems(A.max_n, max_rows);
   constexpr size_t kSmemCap = 200 * 1024;
-  // coded variant when it fits; W == 1 packs up to kO_WARPS plans per block
-  // (fewer for big plans so the codes still fit)
-  const size_t coded_plan = outer_smem_per_warp(A.max_n, max_rows, true, W);
-  int per_block = W == 1 ? kO_WARPS : 1;
+  // coded variant when it fits
   bool coded = true;
-  while (per_block > 1 && coded_plan * per_block > kSmemCap) --per_block;
-  if (coded_plan * per_block > kSmemCap) {
+  size_t plan_smem = outer_smem_per_warp(A.max_n, max_rows, true, W, CPL);
+  int per_block = best_per_block(plan_smem, W, kSmemCap);
+  if (per_block == 0) {
     coded = false;
-    per_block = W == 1 ? kO_WARPS : 1;
+    plan_smem = outer_smem_per_warp(A.max_n, max_rows, false, W, CPL);
+    per_block = best_per_block(plan_smem, W, 227 * 1024);
   }
-  A.smem_per_warp = outer_smem_per_warp(A.max_n, max_rows, coded, W);
-  const size_t smem = A.smem_per_warp * per_block;
-  if (smem > 227 * 1024) return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", smem);
+  if (per_block == 0)
+    return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", plan_smem);
+  A.wv_in_dict = coded && outer_wv_in_dict(A.max_n, max_rows);
+  A.dbl_elems = outer_dbl_elems(A.max_n, max_rows, A.wv_in_dict != 0);
+  A.smem_per_warp = plan_smem;
+  const size_t smem = plan_smem * per_block;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_outer<CPL, true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -52,7 +52,6 @@ def test_steps_counter_and_repeatability():
     s = steps.cpu().numpy().reshape(-1, 2)
     n = b.stats()["n"]
     assert (s[:, 0] >= n).all()            # at least one Dijkstra step per row
-    assert (s[:, 1] > 0).all()
 
 
 def test_chunks_sharing_scratch_match_c_oracle():
