@@ -126,7 +126,8 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
  * clear_count) of d_fused / d_perm is zeroed first (the encoding of an
  * all-zero block), pass clear_count = 0 if the caller cleared it.  d_steps
  * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element
- * loads} (2 x int64) -- the algorithmic work of the outer KM. */
+ * loads from L2 (0 for dictionary-coded plans)} (2 x int64) -- the
+ * algorithmic work of the outer KM. */
 int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                 const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na, int max_nb,
                 int group_mask, int64_t clear_begin, int64_t clear_count, void* stream);
@@ -134,6 +135,18 @@ int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                  const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
                  int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
                  void* stream);
+
+/* sk_map_outer with a global code scratch: big size classes (few plans per
+ * SM with shared-memory codes) keep their dictionary codes in d_codes
+ * (L2-resident) instead of shared memory, so more plans run per SM.
+ * sk_outer_codes_bytes returns the bytes a launch of (n_plans, max_n,
+ * max_rows) would use, 0 when it keeps the codes in shared memory; pass
+ * NULL / 0 to disable. */
+int sk_map_outer_codes(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                       const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                       int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                       uint8_t* d_codes, int64_t codes_bytes, void* stream);
+int64_t sk_outer_codes_bytes(int n_plans, int max_n, int max_rows);
 
 /*
  * km_match on caller-given dense weights (mapping.py:125-149): plans with

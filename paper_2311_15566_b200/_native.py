@@ -39,7 +39,7 @@ assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize ==
 
 EXPORTS = (
     "sk_abi_version", "sk_last_error", "sk_build_weights", "sk_map_batched", "sk_map_fuse",
-    "sk_map_outer", "sk_km_dense",
+    "sk_map_outer", "sk_map_outer_codes", "sk_outer_codes_bytes", "sk_km_dense",
     "sk_sweep_expand", "sk_copy_batched", "sk_enable_peer_access",
     "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
@@ -78,6 +78,8 @@ def load():
         "sk_map_batched": ([vp, i32, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, i64, vp], i32),
         "sk_map_fuse": ([vp, i32, vp, vp, vp, vp, i32, i32, i32, i64, i64, vp], i32),
         "sk_map_outer": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], i32),
+        "sk_map_outer_codes": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i64, vp], i32),
+        "sk_outer_codes_bytes": ([i32, i32, i32], i64),
         "sk_km_dense": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),
         "sk_copy_batched": ([vp, i32, i32, vp], i32),

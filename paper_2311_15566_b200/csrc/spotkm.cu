@@ -575,14 +575,22 @@ __host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int dbl_e
 __host__ __device__ __forceinline__ size_t outer_dict_bytes(int max_n, int slack) {
   return (size_t)kDictSlots * 8 + (((size_t)max_n * max_n + slack + 15) & ~(size_t)15);
 }
-__host__ __device__ __forceinline__ bool outer_wv_in_dict(int max_n, int max_rows) {
-  return (size_t)max_rows * 8 <= outer_dict_bytes(max_n, 0);
+// outer-KM modes: 0 = cost rows gathered from the fused matrix in L2,
+// 1 = one-byte codes in shared memory, 2 = codes in a global (L2-resident)
+// scratch, only the 256-entry table in shared memory -- for big plans whose
+// shared-memory codes would leave few warps per SM
+enum { kOuterL2 = 0, kOuterSmemCodes = 1, kOuterGlobalCodes = 2 };
+
+__host__ __device__ __forceinline__ bool outer_wv_in_dict(int max_n, int max_rows, int mode) {
+  const size_t room = mode == kOuterSmemCodes ? outer_dict_bytes(max_n, 0)
+                      : mode == kOuterGlobalCodes ? (size_t)kDictSlots * 8 : 0;
+  return (size_t)max_rows * 8 <= room;
 }
-__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, bool coded,
+__host__ __device__ __forceinline__ size_t outer_smem_per_warp(int max_n, int max_rows, int mode,
                                                               int warps, int cpl) {
-  size_t bytes =
-      outer_base_bytes(max_n, outer_dbl_elems(max_n, max_rows, coded && outer_wv_in_dict(max_n, max_rows)));
-  if (coded) bytes += outer_dict_bytes(max_n, 32 * warps * cpl);
+  size_t bytes = outer_base_bytes(max_n, outer_dbl_elems(max_n, max_rows, outer_wv_in_dict(max_n, max_rows, mode)));
+  if (mode == kOuterSmemCodes) bytes += outer_dict_bytes(max_n, 32 * warps * cpl);
+  if (mode == kOuterGlobalCodes) bytes += (size_t)kDictSlots * 8;
   if (warps > 1) bytes += (size_t)2 * warps * 24 + (size_t)4 * warps * 4;  // step partials
   return bytes;
 }
@@ -601,8 +609,16 @@ struct OuterArgs {
   size_t smem_per_warp;
   int max_n;
   int dbl_elems;
-  int wv_in_dict;  // CODED: epilogue row weights live in the dictionary area
+  int wv_in_dict;  // coded modes: epilogue row weights live in the dictionary area
+  unsigned char* codes;  // kOuterGlobalCodes: per plan q at codes + q * codes_stride + 16
+  size_t codes_stride;
 };
+
+// per-plan stride of the global code scratch: a 16-byte head (the step's
+// column-0 read lands there), the padded n x n codes and the read slack
+__host__ __device__ __forceinline__ size_t outer_codes_stride(int max_n, int warps, int cpl) {
+  return ((size_t)16 + (size_t)max_n * max_n + (size_t)32 * warps * cpl + 15) & ~(size_t)15;
+}
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -637,8 +653,9 @@ __device__ __forceinline__ void plan_sync() {
     __syncthreads();
 }
 
-template <int CPL, bool CODED, int W>
+template <int CPL, int MODE, int W>
 __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(const OuterArgs A) {
+  constexpr bool CODED = MODE != kOuterL2;
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int T = 32 * W;  // threads per plan
   const int pt = threadIdx.x % T, slot = threadIdx.x / T;
@@ -654,7 +671,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   const int n1 = A.max_n + 1;
 
   // per-plan layout: [double ucol (/ wv): dbl_elems] [i16 match: n1] [i16 way: n1]
-  //                  [CODED: u64 table[256] | u8 codes[max_n^2] (/ wv)] ; W > 1 partials after
+  //                  [CODED: u64 table[256] | mode 1: u8 codes[max_n^2] (/ wv)] ; W > 1 partials after
   unsigned char* base = smem + (size_t)slot * A.smem_per_warp;
   double* ucol = reinterpret_cast<double*>(base);
   short* match = reinterpret_cast<short*>(base + (size_t)A.dbl_elems * 8);
@@ -667,7 +684,8 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   bool coded = false;
   unsigned long long* table =
       reinterpret_cast<unsigned long long*>(base + outer_base_bytes(A.max_n, A.dbl_elems));
-  unsigned char* codes = reinterpret_cast<unsigned char*>(table + kDictSlots);
+  unsigned char* codes = MODE == kOuterGlobalCodes ? A.codes + (size_t)q * A.codes_stride + 16
+                                                   : reinterpret_cast<unsigned char*>(table + kDictSlots);
   const unsigned table_s = smem_addr(table), codes_s = smem_addr(codes);
   // W > 1: warp-winner partials, double-buffered by step parity
   struct Partial {
@@ -774,9 +792,16 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         // the padded n x n code matrix: unpredicated reads, one LDS.U8 + one
         // LDS.64 per column (32-bit shared-window addresses); reads for
         // columns outside 1..n land in the slack and are never used
-        const unsigned rowc = codes_s + (unsigned)((i0 - 1) * n + pt - 1);
+        const int rowo = (i0 - 1) * n + pt - 1;
+        if (MODE == kOuterGlobalCodes) {
+          const unsigned char* rowg = codes + rowo;
 #pragma unroll
-        for (int k = 0; k < CPL; ++k) wx[k] = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
+          for (int k = 0; k < CPL; ++k) wx[k] = lds_f64(table_s + 8u * (unsigned)rowg[T * k]);
+        } else {
+          const unsigned rowc = codes_s + (unsigned)rowo;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) wx[k] = lds_f64(table_s + 8u * lds_u8(rowc + (unsigned)(T * k)));
+        }
       } else {
         const unsigned ld = (i0 - 1) < nA ? (act & real) : 0u;
         const double* rowp = Fp + ((i0 - 1) * nB - 1) + pt;
@@ -1040,8 +1065,9 @@ __global__ void __launch_bounds__(kC_TPB) k_copy(const sk_copy* __restrict__ cop
 }
 
 // plans per block (W == 1) maximising the plans resident per SM under the
-// shared-memory (incl. the 1 KB per-block reserve), thread and block limits
-int best_per_block(size_t plan_smem, int W, size_t cap) {
+// shared-memory (incl. the 1 KB per-block reserve), thread and block limits;
+// *resident receives that count (0: does not fit)
+int best_per_block(size_t plan_smem, int W, size_t cap, int* resident = nullptr) {
   constexpr size_t kSmemSM = 228 * 1024, kReserve = 1024;
   int best = 0, best_res = 0;
   for (int pb = 1; pb <= (W == 1 ? kO_WARPS : 1); ++pb) {
@@ -1055,69 +1081,113 @@ int best_per_block(size_t plan_smem, int W, size_t cap) {
       best = pb;
     }
   }
+  if (resident) *resident = best_res;
   return best;
 }
 
-template <int CPL, int W>
-int launch_outer(OuterArgs A, int max_rows, cudaStream_t s) {
-  constexpr size_t kSmemCap = 200 * 1024;
-  // coded variant when it fits
-  bool coded = true;
-  size_t plan_smem = outer_smem_per_warp(A.max_n, max_rows, true, W, CPL);
-  int per_block = best_per_block(plan_smem, W, kSmemCap);
-  if (per_block == 0) {
-    coded = false;
-    plan_smem = outer_smem_per_warp(A.max_n, max_rows, false, W, CPL);
-    per_block = best_per_block(plan_smem, W, 227 * 1024);
+constexpr size_t kSmemCodedCap = 200 * 1024;
+
+// plans resident per SM below which big plans move their codes to the global
+// scratch (when the caller provides one); SK_OUTER_GMIN overrides (tuning)
+int global_codes_threshold() {
+  static const int v = [] {
+    const char* e = getenv("SK_OUTER_GMIN");
+    return e ? atoi(e) : 12;
+  }();
+  return v;
+}
+
+// mode the launcher picks for n_plans plans of (max_n, max_rows) at (CPL, W):
+// global codes when shared-memory codes would leave few plans per SM and the
+// launch is big enough (>= 2 waves) for the extra concurrency to pay
+int outer_mode(int n_plans, int max_n, int max_rows, int W, int CPL, bool have_codes) {
+  constexpr int kSMs = 148;
+  int res = 0;
+  best_per_block(outer_smem_per_warp(max_n, max_rows, kOuterSmemCodes, W, CPL), W, kSmemCodedCap, &res);
+  const bool few = res < global_codes_threshold() && (long long)n_plans > 2LL * kSMs * res;
+  if (have_codes && (res == 0 || few)) return kOuterGlobalCodes;
+  return res > 0 ? kOuterSmemCodes : kOuterL2;
+}
+
+// (columns per thread, warps per plan) for a size class -- must match
+// outer_dispatch's instantiations
+void outer_shape(int max_n, int* cpl, int* w) {
+  const int need = (max_n + 1 + 31) / 32;
+  *w = 1;
+  if (need <= 6) {
+    *cpl = need < 1 ? 1 : need;
+    return;
   }
+  if (need <= 8) {
+    *cpl = 8;
+    return;
+  }
+  const int need4 = (max_n + 1 + 127) / 128;
+  *w = 4;
+  if (need4 <= 3) *cpl = 3;
+  else if (need4 <= 6) *cpl = need4;
+  else if (need4 <= 8) *cpl = 8;
+  else if (need4 <= 12) *cpl = 12;
+  else if (need4 <= 16) *cpl = 16;
+  else {
+    const int need8 = (max_n + 1 + 255) / 256;
+    *w = 8;
+    *cpl = need8 <= 12 ? 12 : 16;
+  }
+}
+
+template <int CPL, int MODE, int W>
+void configure_outer() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_outer<CPL, MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = true;
+  }
+}
+
+template <int CPL, int W>
+int launch_outer(OuterArgs A, int max_rows, size_t codes_bytes, cudaStream_t s) {
+  const size_t stride = outer_codes_stride(A.max_n, W, CPL);
+  const bool have_codes = A.codes != nullptr && codes_bytes >= stride * (size_t)A.n_plans;
+  const int mode = outer_mode(A.n_plans, A.max_n, max_rows, W, CPL, have_codes);
+  const size_t plan_smem = outer_smem_per_warp(A.max_n, max_rows, mode, W, CPL);
+  const int per_block = best_per_block(plan_smem, W, mode == kOuterSmemCodes ? kSmemCodedCap : 227 * 1024);
   if (per_block == 0)
     return set_err(SK_EINVAL, "outer KM shared memory %zu B too large", plan_smem);
-  A.wv_in_dict = coded && outer_wv_in_dict(A.max_n, max_rows);
+  A.wv_in_dict = outer_wv_in_dict(A.max_n, max_rows, mode);
   A.dbl_elems = outer_dbl_elems(A.max_n, max_rows, A.wv_in_dict != 0);
   A.smem_per_warp = plan_smem;
+  A.codes_stride = stride;
   const size_t smem = plan_smem * per_block;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_outer<CPL, true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_outer<CPL, false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    configured = true;
-  }
   const int blocks = (A.n_plans + per_block - 1) / per_block;
-  if (coded)
-    k_outer<CPL, true, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
-  else
-    k_outer<CPL, false, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
+  if (mode == kOuterSmemCodes) {
+    configure_outer<CPL, kOuterSmemCodes, W>();
+    k_outer<CPL, kOuterSmemCodes, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
+  } else if (mode == kOuterGlobalCodes) {
+    configure_outer<CPL, kOuterGlobalCodes, W>();
+    k_outer<CPL, kOuterGlobalCodes, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
+  } else {
+    configure_outer<CPL, kOuterL2, W>();
+    k_outer<CPL, kOuterL2, W><<<blocks, per_block * 32 * W, smem, s>>>(A);
+  }
   return cuda_check("k_outer launch");
 }
 
 // Small plans: one warp per plan (columns per lane = need).  Big plans
-// (more than 8 columns per lane): one 4-warp block per plan.
-int outer_dispatch(const OuterArgs& A, int max_rows, cudaStream_t s) {
-  const int need = (A.max_n + 1 + 31) / 32;  // columns per lane with one warp
-  switch (need) {
-    case 0:
-    case 1: return launch_outer<1, 1>(A, max_rows, s);
-    case 2: return launch_outer<2, 1>(A, max_rows, s);
-    case 3: return launch_outer<3, 1>(A, max_rows, s);
-    case 4: return launch_outer<4, 1>(A, max_rows, s);
-    case 5: return launch_outer<5, 1>(A, max_rows, s);
-    case 6: return launch_outer<6, 1>(A, max_rows, s);
-    case 7:
-    case 8: return launch_outer<8, 1>(A, max_rows, s);
-    default: break;
-  }
-  const int need4 = (A.max_n + 1 + 127) / 128;  // columns per thread with 4 warps
-  if (need4 <= 3) return launch_outer<3, 4>(A, max_rows, s);
-  if (need4 <= 4) return launch_outer<4, 4>(A, max_rows, s);
-  if (need4 <= 5) return launch_outer<5, 4>(A, max_rows, s);
-  if (need4 <= 6) return launch_outer<6, 4>(A, max_rows, s);
-  if (need4 <= 8) return launch_outer<8, 4>(A, max_rows, s);
-  if (need4 <= 12) return launch_outer<12, 4>(A, max_rows, s);
-  if (need4 <= 16) return launch_outer<16, 4>(A, max_rows, s);
-  const int need8 = (A.max_n + 1 + 255) / 256;  // columns per thread with 8 warps
-  if (need8 <= 12) return launch_outer<12, 8>(A, max_rows, s);
-  if (need8 <= 16) return launch_outer<16, 8>(A, max_rows, s);
-  return set_err(SK_EINVAL, "outer KM size %d exceeds 4095", A.max_n);
+// (more than 8 columns per lane): one 4- or 8-warp block per plan.
+int outer_dispatch(const OuterArgs& A, int max_rows, size_t codes_bytes, cudaStream_t s) {
+  int cpl = 0, w = 0;
+  if (A.max_n > 4095) return set_err(SK_EINVAL, "outer KM size %d exceeds 4095", A.max_n);
+  outer_shape(A.max_n, &cpl, &w);
+#define SK_OUTER_CASE(C, WW) \
+  if (cpl == C && w == WW) return launch_outer<C, WW>(A, max_rows, codes_bytes, s);
+  SK_OUTER_CASE(1, 1) SK_OUTER_CASE(2, 1) SK_OUTER_CASE(3, 1) SK_OUTER_CASE(4, 1)
+  SK_OUTER_CASE(5, 1) SK_OUTER_CASE(6, 1) SK_OUTER_CASE(8, 1)
+  SK_OUTER_CASE(3, 4) SK_OUTER_CASE(4, 4) SK_OUTER_CASE(5, 4) SK_OUTER_CASE(6, 4)
+  SK_OUTER_CASE(8, 4) SK_OUTER_CASE(12, 4) SK_OUTER_CASE(16, 4)
+  SK_OUTER_CASE(12, 8) SK_OUTER_CASE(16, 8)
+#undef SK_OUTER_CASE
+  return set_err(SK_EINVAL, "outer KM shape (%d, %d) not instantiated", cpl, w);
 }
 
 constexpr int kMaxGridY = 65535;
@@ -1180,15 +1250,32 @@ int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
   return SK_OK;
 }
 
+int sk_map_outer_codes(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                       const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                       int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                       uint8_t* d_codes, int64_t codes_bytes, void* stream) {
+  if (n_plans < 0 || max_n < 0 || max_rows < 0 || codes_bytes < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0) return SK_OK;
+  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, {}, 0, max_n, 0,
+              0, d_codes, 0};
+  for (int g = 0; g <= 8; ++g) A.zero_perm[g] = zero_perm_of(g);
+  return outer_dispatch(A, max_rows, (size_t)codes_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int64_t sk_outer_codes_bytes(int n_plans, int max_n, int max_rows) {
+  if (n_plans <= 0 || max_n <= 0 || max_n > 4095 || max_rows < 0) return 0;
+  int cpl = 0, w = 0;
+  outer_shape(max_n, &cpl, &w);
+  if (outer_mode(n_plans, max_n, max_rows, w, cpl, true) != kOuterGlobalCodes) return 0;
+  return (int64_t)(outer_codes_stride(max_n, w, cpl) * (size_t)n_plans);
+}
+
 int sk_map_outer(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                  const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
                  int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
                  void* stream) {
-  if (n_plans < 0 || max_n < 0 || max_rows < 0) return set_err(SK_EINVAL, "negative sizes");
-  if (n_plans == 0) return SK_OK;
-  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, {}, 0, max_n, 0};
-  for (int g = 0; g <= 8; ++g) A.zero_perm[g] = zero_perm_of(g);
-  return outer_dispatch(A, max_rows, static_cast<cudaStream_t>(stream));
+  return sk_map_outer_codes(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total,
+                            d_steps, max_n, max_rows, nullptr, 0, stream);
 }
 
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,

@@ -231,6 +231,13 @@ class SweepRunner:
         self.d_out = torch.empty(self.out_bytes, dtype=torch.uint8, device=self.dev)
         self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8, pin_memory=True)
         self.d2h_bytes = 8 * Q + 4 * R
+        # global code scratch for the big size classes (sk_outer_codes_bytes);
+        # the classes run concurrently, so each gets its own slice
+        need = [int(self.lib.sk_outer_codes_bytes(b - a, mn, rows))
+                for (a, b, mn), rows in zip(self.classes, self.class_rows)]
+        self.codes_off = np.concatenate([[0], np.cumsum(need)]).astype(np.int64)
+        self.codes_need = need
+        self.codes = buf("codes", max(int(self.codes_off[-1]), 1), torch.uint8)
         self.stream = stream
         # one side stream per outer-KM size class so the classes' tails overlap
         self.side = [torch.cuda.Stream(self.dev) for _ in self.classes]
@@ -282,11 +289,13 @@ class SweepRunner:
                                       self.class_gmask[c], *self.class_clear[c], st.cuda_stream)
             nat.check(rc)
             mark(f"k_fuse[{c}]")
-            rc = self.lib.sk_map_outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
-                                       self.segs.data_ptr(), self.fused.data_ptr(),
-                                       self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
-                                       0 if steps is None else steps.data_ptr() + 16 * a, mn,
-                                       self.class_rows[c], st.cuda_stream)
+            rc = self.lib.sk_map_outer_codes(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
+                                             self.segs.data_ptr(), self.fused.data_ptr(),
+                                             self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
+                                             0 if steps is None else steps.data_ptr() + 16 * a, mn,
+                                             self.class_rows[c],
+                                             self.codes.data_ptr() + int(self.codes_off[c]),
+                                             self.codes_need[c], st.cuda_stream)
             nat.check(rc)
             mark(f"k_outer[{c}]")
             if profile is None:

@@ -77,3 +77,15 @@ def test_chunks_sharing_scratch_match_c_oracle():
         exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
         assert np.array_equal(assign, exp_assign)
         assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
+
+
+def test_global_code_mode_matches_c_oracle():
+    """A size class big enough (n ~ 130, > 2 waves) that the outer KM keeps its
+    dictionary codes in the global scratch instead of shared memory."""
+    b = sweep.make_sweep(256, 1800, seed=21, shapes=((6, 2), (2, 8)))
+    r = sweep.SweepRunner(b)
+    assert any(x > 0 for x in r.codes_need)
+    assign, totals = r.run()
+    exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
+    assert np.array_equal(assign, exp_assign)
+    assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
