@@ -15,7 +15,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 def header_symbols():
     text = (ROOT / "include" / "spotkm.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void|double)\s+(sk_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*|void|double)\s+(sk_\w+)\s*\(",
                                  text, re.M)))
 
 
