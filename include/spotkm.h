@@ -121,10 +121,11 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
                    int max_rows, int group_mask, int64_t fused_elems, void* stream);
 
 /* The two halves of sk_map_batched, for callers that time or pipeline them:
- * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  K2a only
- * visits fused pairs that can be non-zero; [clear_begin, clear_begin +
- * clear_count) of d_fused / d_perm is zeroed first (the encoding of an
- * all-zero block), pass clear_count = 0 if the caller cleared it.  d_steps
+ * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  K2a
+ * writes every element of each plan's fused matrix (zero rows first, then
+ * only the fused pairs that can be non-zero); [clear_begin, clear_begin +
+ * clear_count) of d_fused / d_perm is additionally memset to zero first --
+ * not needed, pass clear_count = 0.  d_steps
  * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element
  * loads from L2 (0 for dictionary-coded plans)} (2 x int64) -- the
  * algorithmic work of the outer KM. */

@@ -348,9 +348,10 @@ __device__ __forceinline__ FusedBlock fuse_block(const sk_plan& p, int a, const 
   return out;
 }
 
-// One lane group (LPG lanes) per fused GPU group a.  The fused matrix and
-// perm buffers are cleared beforehand (F = 0.0, perm = 0 meaning "zero-matrix
-// permutation"), so only pairs (a, b) that CAN be non-zero are visited: the
+// One lane group (LPG lanes) per fused GPU group a.  The group first writes
+// its whole fused row as zeros (F = 0.0, perm = 0 meaning "zero-matrix
+// permutation"; coalesced full sectors, no separate clear and no partial-
+// sector fills), then visits only pairs (a, b) that CAN be non-zero: the
 // lanes reduce the group's layer span [L0, L1) over its segments, and per new
 // pipeline d only the fused slots of stages overlapping that span are
 // candidates (a contiguous run of b).  Every other block is all-zero by
@@ -418,6 +419,16 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   pm_over = __any_sync(kFull, pm_over);
   lo = max(lo, 0);
   hi = min(hi, p.L);
+  // the group writes its whole fused row: zeros first (coalesced, full
+  // sectors -- the encoding of an all-zero block), then the candidate blocks
+  const long long row0 = p.f_off + (long long)a * nB;
+  if (live) {
+    for (int b = sub; b < nB; b += LPG) {
+      F[row0 + b] = 0.0;
+      perm[row0 + b] = 0u;
+    }
+  }
+  __syncwarp();
   if (!live || lo >= hi) return;  // the whole row group is zero
   const int p_lo = stage_of(lo, p.L, p.P), p_hi = stage_of(hi - 1, p.L, p.P);
   const int span = ((p_hi + 1 - p_lo) * p.M) / G;  // fused slots per pipeline
@@ -444,7 +455,6 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   // (named pipeline, offset)
   const int nbits = __popcll(pm0) + __popcll(pm1);
   const int n_items = span * (1 + nbits);
-  const long long row0 = p.f_off + (long long)a * nB;
   for (int it = sub; it < n_items; it += LPG) {
     int o = it, dq = -1;  // dq: 0-based named pipeline, -1 = model only
     if (it >= span) {
@@ -1282,8 +1292,9 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
                    const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int32_t* d_assign,
                    double* d_total, int max_na, int max_nb, int max_rows, int group_mask,
                    int64_t fused_elems, void* stream) {
+  (void)fused_elems;  // k_fuse writes every fused element itself
   int rc = sk_map_fuse(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, max_na, max_nb,
-                       group_mask, 0, fused_elems, stream);
+                       group_mask, 0, 0, stream);
   if (rc) return rc;
   const int max_n = max_na > max_nb ? max_na : max_nb;
   return sk_map_outer(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, nullptr,

@@ -119,7 +119,7 @@ class MapBatch:
         p_assign = p_total + 8 * Q
         st = _stream_ptr()
         rc = lib.sk_map_fuse(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
-                             info["max_na"], info["max_nb"], info["gmask"], 0, info["pairs"], st)
+                             info["max_na"], info["max_nb"], info["gmask"], 0, 0, st)
         nat.check(rc, mapping_error)
         ns = np.array([n_of[q] for q in order], dtype=np.int64)
         for a, b, mn in outer_classes(ns):

@@ -193,8 +193,6 @@ class SweepRunner:
         self.classes = outer_classes(st["n"])
         self.class_rows = [int(st["rows"][a:b].max()) for a, b, _ in self.classes]
         f_off = batch.plans["f_off"].astype(np.int64)
-        self.class_clear = [(int(f_off[a]), int(f_off[b - 1] + st["pairs"][b - 1] - f_off[a]))
-                            for a, b, _ in self.classes]
         self.class_na = [int(st["nA"][a:b].max()) for a, b, _ in self.classes]
         self.class_nb = [int(st["nB"][a:b].max()) for a, b, _ in self.classes]
         self.class_gmask = [int(np.bitwise_or.reduce(1 << batch.plans["group"][a:b].astype(np.int64)))
@@ -286,7 +284,7 @@ class SweepRunner:
             rc = self.lib.sk_map_fuse(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
                                       self.segs.data_ptr(), self.fused.data_ptr(),
                                       self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
-                                      self.class_gmask[c], *self.class_clear[c], st.cuda_stream)
+                                      self.class_gmask[c], 0, 0, st.cuda_stream)
             nat.check(rc)
             mark(f"k_fuse[{c}]")
             rc = self.lib.sk_map_outer_codes(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),

@@ -43,6 +43,9 @@ def test_steps_counter_and_repeatability():
     r = sweep.SweepRunner(b)
     a1, t1 = r.run()
     steps = torch.zeros(2 * b.n_plans, dtype=torch.int64, device="cuda")
+    # k_fuse writes every fused element itself: stale scratch must not matter
+    r.fused.fill_(float("nan"))
+    r.perm.fill_(-1)
     r.upload()
     r.solve(steps=steps)
     r.download()
