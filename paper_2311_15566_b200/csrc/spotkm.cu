@@ -21,6 +21,7 @@
 #include <stdarg.h>
 #include <stdlib.h>
 #include <stdint.h>
+#include <type_traits>
 #include <stdio.h>
 
 #include "../../include/spotkm.h"
@@ -684,8 +685,8 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   //                  [CODED: u64 table[256] | mode 1: u8 codes[max_n^2] (/ wv)] ; W > 1 partials after
   unsigned char* base = smem + (size_t)slot * A.smem_per_warp;
   double* ucol = reinterpret_cast<double*>(base);
-  short* match = reinterpret_cast<short*>(base + (size_t)A.dbl_elems * 8);
-  short* way = match + n1;
+  unsigned short* match = reinterpret_cast<unsigned short*>(base + (size_t)A.dbl_elems * 8);
+  unsigned short* way = match + n1;
 
   const double* Fp = A.F + p.f_off;
   // dictionary-code the fused matrix into shared memory (CODED variant).
@@ -786,19 +787,22 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
 
   int nsteps = 0, nloads = 0;  // nloads: uncoded path only
   int parity = 0;
+  // the row loop, instantiated once per cost-row source so the Dijkstra step
+  // carries no per-step branch on whether the dictionary build succeeded
+  auto km_rows = [&](auto use_codes) {
+  constexpr bool UC = decltype(use_codes)::value;
   for (int i = 1; i <= n; ++i) {
     unsigned used = (pt == 0) ? 1u : 0u;  // column 0
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
     int j0 = 0;
     while (true) {
-      ++nsteps;
       const int i0 = match[j0];
       const double ui0 = ucol[j0];
       const unsigned act = valid & ~used;
       // the row's weights w (cost = -w; padded entries are 0.0 -> cost -0.0)
       double wx[CPL];
-      if (CODED && coded) {
+      if constexpr (UC) {
         // the padded n x n code matrix: unpredicated reads, one LDS.U8 + one
         // LDS.64 per column (32-bit shared-window addresses); reads for
         // columns outside 1..n land in the slack and are never used
@@ -915,11 +919,13 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       if ((unsigned)j0 % (unsigned)T == (unsigned)pt) used |= 1u << ((unsigned)j0 / (unsigned)T);
       if (match[j0] == 0) break;
     }
+    // every step marked one column used: the row's step count
+    if (A.steps) nsteps += __popc(used) - (pt == 0 ? 1 : 0);
     // publish predecessors, then walk the augmenting path (one thread), then
     // seed the next row
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
-      if (((used | valid) >> k) & 1u) way[pt + T * k] = (short)wr[k];
+      if (((used | valid) >> k) & 1u) way[pt + T * k] = (unsigned short)wr[k];
     plan_sync<W>();
     if (pt == 0) {
       while (j0) {
@@ -928,16 +934,21 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         ucol[j0] = ucol[j1];
         j0 = j1;
       }
-      match[0] = (short)(i + 1);
+      match[0] = (unsigned short)(i + 1);
       ucol[0] = 0.0;
     }
     plan_sync<W>();
   }
+  };
+  if (CODED && coded)
+    km_rows(std::true_type{});
+  else
+    km_rows(std::false_type{});
 
   // row_to_col for real fused rows -> way[] (free now)
   for (int j = pt + 1; j <= n; j += T) {
     const int r = match[j];
-    if (r >= 1 && r <= nA) way[r - 1] = (short)(j - 1);
+    if (r >= 1 && r <= nA) way[r - 1] = (unsigned short)(j - 1);
   }
   plan_sync<W>();
   double* wv = (CODED && A.wv_in_dict) ? reinterpret_cast<double*>(table) : ucol;
@@ -962,15 +973,22 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   plan_sync<W>();
   if (A.steps) {
 #pragma unroll
-    for (int off = 16; off; off >>= 1) nloads += __shfl_xor_sync(kFull, nloads, off);  // < 2^31 per plan
-    if (pt == 0) A.steps[2 * q] = nsteps;
+    for (int off = 16; off; off >>= 1) {  // < 2^31 per plan
+      nloads += __shfl_xor_sync(kFull, nloads, off);
+      nsteps += __shfl_xor_sync(kFull, nsteps, off);
+    }
     if (W == 1) {
-      if (lane == 0) A.steps[2 * q + 1] = nloads;
+      if (lane == 0) {
+        A.steps[2 * q] = nsteps;
+        A.steps[2 * q + 1] = nloads;
+      }
     } else {
-      if (pt == 0) A.steps[2 * q + 1] = 0;
+      if (pt == 0) A.steps[2 * q] = A.steps[2 * q + 1] = 0;
       __syncthreads();
-      if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A.steps + 2 * q + 1),
-                               (unsigned long long)nloads);
+      if (lane == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.steps + 2 * q), (unsigned long long)nsteps);
+        atomicAdd(reinterpret_cast<unsigned long long*>(A.steps + 2 * q + 1), (unsigned long long)nloads);
+      }
     }
   }
   if (pt == 0) {
