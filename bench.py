@@ -498,7 +498,7 @@ def run_ours(args):
     geom, shapes = sweep.MODELS[args.model]
     batch = sweep.make_sweep(args.positions, args.sets, seed=1000 + rank, model=geom, shapes=shapes)
     runner = sweep.SweepRunner(batch)
-    per_step_launches = 1 + sum(bin(m).count("1") for m in runner.class_gmask) + len(runner.classes)
+    per_step_launches = runner.launches_per_solve
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     K, W = args.steps, args.warmup
     dev_ms, e2e_ms, clk, launches = measure_ours(runner, K, W, world, rank, local, flush,

@@ -240,6 +240,16 @@ class SweepRunner:
         # one side stream per outer-KM size class so the classes' tails overlap
         self.side = [torch.cuda.Stream(self.dev) for _ in self.classes]
 
+    @property
+    def launches_per_solve(self) -> int:
+        """Kernel launches of one solve(): expand and fuse split the plans into
+        chunks of at most 65,535 (grid y); one fuse launch per group size."""
+        ch = lambda q: -(-q // 65535)  # noqa: E731
+        n = ch(self.b.n_plans)
+        for (a, b, _), m in zip(self.classes, self.class_gmask):
+            n += bin(m).count("1") * ch(b - a) + 1
+        return n
+
     def _s(self) -> int:
         return (self.stream or torch.cuda.current_stream(self.dev)).cuda_stream
 
