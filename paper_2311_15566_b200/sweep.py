@@ -229,6 +229,12 @@ class SweepRunner:
         self.d_out = torch.empty(self.out_bytes, dtype=torch.uint8, device=self.dev)
         self.h_out = torch.empty(self.out_bytes, dtype=torch.uint8, pin_memory=True)
         self.d2h_bytes = 8 * Q + 4 * R
+        # per class: the byte ranges of its totals and assignments in d_out
+        rb = batch.plans["row_base"].astype(np.int64)
+        rows = batch.plans["rows"].astype(np.int64)
+        self._class_out = [((8 * a, 8 * b),
+                            (8 * Q + 4 * int(rb[a]), 8 * Q + 4 * int(rb[b - 1] + rows[b - 1])))
+                           for a, b, _ in self.classes]
         # global code scratch for the big size classes (sk_outer_codes_bytes);
         # the classes run concurrently, so each gets its own slice
         need = [int(self.lib.sk_outer_codes_bytes(b - a, mn, rows))
@@ -256,7 +262,7 @@ class SweepRunner:
     def upload(self):
         self.d_in.copy_(self.h_in, non_blocking=True)
 
-    def solve(self, steps=None, profile=None):
+    def solve(self, steps=None, profile=None, download: bool = False):
         """One pass of the hot path on the runner's stream: expand, then per
         outer-KM size class the fused inner KMs and the outer KM, each class
         on its own stream so the classes' tails overlap.
@@ -264,7 +270,9 @@ class SweepRunner:
         steps: optional int64 device tensor [2*Q] receiving {Dijkstra steps,
         cost loads} per plan.  profile: optional dict; when given, the launches
         are serialised on the main stream and bracketed with CUDA events so
-        per-kernel times can be read back (profile["events"])."""
+        per-kernel times can be read back (profile["events"]).  download: also
+        copy each class's results to the pinned host buffer on its stream as
+        soon as its outer KM ends (overlaps the D2H with the other classes)."""
         base = self.d_in.data_ptr()
         p_desc, p_plans, p_alive, p_tok = (base + o for o in self.offs)
         Q = self.b.n_plans
@@ -306,6 +314,10 @@ class SweepRunner:
                                              self.codes_need[c], st.cuda_stream)
             nat.check(rc)
             mark(f"k_outer[{c}]")
+            if download:
+                with torch.cuda.stream(st):
+                    for lo, hi in self._class_out[c]:
+                        self.h_out[lo:hi].copy_(self.d_out[lo:hi], non_blocking=True)
             if profile is None:
                 done = torch.cuda.Event()
                 done.record(side)
@@ -335,7 +347,6 @@ class SweepRunner:
 
     def run(self):
         self.upload()
-        self.solve()
-        self.download()
+        self.solve(download=True)
         torch.cuda.current_stream(self.dev).synchronize()
         return self.results()
