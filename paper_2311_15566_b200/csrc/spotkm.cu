@@ -546,9 +546,11 @@ int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, 
 // ---------------------------------------------------------------------------
 // K2b: outer KM, one warp per plan.
 //
-// Column j (0..n) is owned by lane j % 32, slot k = j / 32.  The owner keeps
-// the column's slack minv[j], potential v[j], predecessor way[j] and used bit
-// in registers.  Row potentials are kept per COLUMN (ucol[j] = u[match[j]],
+// Column j (1..n) is owned by thread (j - 1) % T, slot k = (j - 1) / T (T =
+// threads per plan); the reference's virtual column 0 has no slot (it is
+// always used; only its row potential, ucol[0], is ever read).  The owner
+// keeps the column's slack minv[j], potential v[j], predecessor way[j] and
+// used bit in registers.  Row potentials are kept per COLUMN (ucol[j] = u[match[j]],
 // shared memory): the reference only ever reads u[i0] with i0 = match[j0]
 // and adds delta to u[match[j]] for used j, so indexing by column removes the
 // match[] indirection from the step's critical path; the augmenting walk
@@ -766,7 +768,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   unsigned valid = 0u, real = 0u;
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
-    const int j = pt + T * k;
+    const int j = 1 + pt + T * k;  // the virtual column 0 has no slot
     if (j >= 1 && j <= n) valid |= 1u << k;
     if (j >= 1 && j <= nB) real |= 1u << k;
   }
@@ -792,7 +794,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   auto km_rows = [&](auto use_codes) {
   constexpr bool UC = decltype(use_codes)::value;
   for (int i = 1; i <= n; ++i) {
-    unsigned used = (pt == 0) ? 1u : 0u;  // column 0
+    unsigned used = 0u;  // slot columns; column 0 (always used) is implicit
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
     int j0 = 0;
@@ -806,7 +808,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         // the padded n x n code matrix: unpredicated reads, one LDS.U8 + one
         // LDS.64 per column (32-bit shared-window addresses); reads for
         // columns outside 1..n land in the slack and are never used
-        const int rowo = (i0 - 1) * n + pt - 1;
+        const int rowo = (i0 - 1) * n + pt;
         if (MODE == kOuterGlobalCodes) {
           const unsigned char* rowg = codes + rowo;
 #pragma unroll
@@ -818,7 +820,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         }
       } else {
         const unsigned ld = (i0 - 1) < nA ? (act & real) : 0u;
-        const double* rowp = Fp + ((i0 - 1) * nB - 1) + pt;
+        const double* rowp = Fp + (i0 - 1) * nB + pt;
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
           double x = 0.0;
@@ -842,7 +844,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         best = better ? minv[k] : best;
         bk = better ? k : bk;
       }
-      const unsigned bj = (best < kInf) ? (unsigned)(pt + T * bk) : 0xffffffffu;
+      const unsigned bj = (best < kInf) ? (unsigned)(1 + pt + T * bk) : 0xffffffffu;
       unsigned jw;
       double delta;
       // fast path (~90% of steps on real plans): no negative slack and some
@@ -882,7 +884,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
       const bool c2 = c1 && (unsigned)key == lo;
       jw = __reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
-      delta = __shfl_sync(kFull, best, (jw % T) & 31);
+      delta = __shfl_sync(kFull, best, ((jw - 1) % T) & 31);
       if (W > 1) {
         Partial* pp = partial + parity * W;
         if (lane == 0) pp[pw] = {((unsigned long long)hi << 32) | lo, delta, jw, 0u};
@@ -908,24 +910,25 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       // non-zero result can observe), so the update is skipped
       if (delta != 0.0) {
 #pragma unroll
+        if (pt == 0) ucol[0] += delta;  // column 0: the current row's u
         for (int k = 0; k < CPL; ++k) {
           const bool u = (used >> k) & 1u;
-          if (u) ucol[pt + T * k] += delta;
+          if (u) ucol[1 + pt + T * k] += delta;
           v[k] = u ? v[k] - delta : v[k];
           minv[k] = (!u && ((valid >> k) & 1u)) ? minv[k] - delta : minv[k];
         }
       }
       j0 = j1;
-      if ((unsigned)j0 % (unsigned)T == (unsigned)pt) used |= 1u << ((unsigned)j0 / (unsigned)T);
+      if ((unsigned)(j0 - 1) % (unsigned)T == (unsigned)pt) used |= 1u << ((unsigned)(j0 - 1) / (unsigned)T);
       if (match[j0] == 0) break;
     }
     // every step marked one column used: the row's step count
-    if (A.steps) nsteps += __popc(used) - (pt == 0 ? 1 : 0);
+    if (A.steps) nsteps += __popc(used);
     // publish predecessors, then walk the augmenting path (one thread), then
     // seed the next row
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
-      if (((used | valid) >> k) & 1u) way[pt + T * k] = (unsigned short)wr[k];
+      if (((used | valid) >> k) & 1u) way[1 + pt + T * k] = (unsigned short)wr[k];
     plan_sync<W>();
     if (pt == 0) {
       while (j0) {
@@ -1140,7 +1143,7 @@ int outer_mode(int n_plans, int max_n, int max_rows, int W, int CPL, bool have_c
 // (columns per thread, warps per plan) for a size class -- must match
 // outer_dispatch's instantiations
 void outer_shape(int max_n, int* cpl, int* w) {
-  const int need = (max_n + 1 + 31) / 32;
+  const int need = (max_n + 31) / 32;  // columns 1..n over the slots
   *w = 1;
   if (need <= 6) {
     *cpl = need < 1 ? 1 : need;
@@ -1150,7 +1153,7 @@ void outer_shape(int max_n, int* cpl, int* w) {
     *cpl = 8;
     return;
   }
-  const int need4 = (max_n + 1 + 127) / 128;
+  const int need4 = (max_n + 127) / 128;
   *w = 4;
   if (need4 <= 3) *cpl = 3;
   else if (need4 <= 6) *cpl = need4;
@@ -1158,7 +1161,7 @@ void outer_shape(int max_n, int* cpl, int* w) {
   else if (need4 <= 12) *cpl = 12;
   else if (need4 <= 16) *cpl = 16;
   else {
-    const int need8 = (max_n + 1 + 255) / 256;
+    const int need8 = (max_n + 255) / 256;
     *w = 8;
     *cpl = need8 <= 12 ? 12 : 16;
   }

@@ -141,16 +141,16 @@ def _align(n: int, a: int = 256) -> int:
 def cpl_bucket(n: int):
     """(warps per plan, columns per thread) of the outer-KM template the
     dispatch picks for size n (mirrors outer_dispatch in spotkm.cu)."""
-    need = max(1, (n + 1 + 31) // 32)
+    need = max(1, (n + 31) // 32)
     if need <= 6:
         return (1, need)
     if need <= 8:
         return (1, 8)
-    need4 = (n + 1 + 127) // 128
+    need4 = (n + 127) // 128
     for c in (3, 4, 5, 6, 8, 12, 16):
         if need4 <= c:
             return (4, c)
-    need8 = (n + 1 + 255) // 256
+    need8 = (n + 255) // 256
     return (8, 12) if need8 <= 12 else (8, 16)
 
 

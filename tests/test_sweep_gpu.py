@@ -85,7 +85,7 @@ def test_chunks_sharing_scratch_match_c_oracle():
 def test_global_code_mode_matches_c_oracle():
     """A size class big enough (n ~ 130, > 2 waves) that the outer KM keeps its
     dictionary codes in the global scratch instead of shared memory."""
-    b = sweep.make_sweep(256, 1800, seed=21, shapes=((6, 2), (2, 8)))
+    b = sweep.make_sweep(256, 2600, seed=21, shapes=((6, 2), (2, 8)))
     r = sweep.SweepRunner(b)
     assert any(x > 0 for x in r.codes_need)
     assign, totals = r.run()
