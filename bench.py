@@ -215,9 +215,11 @@ def cpu_c_rate(batch, cores: int, seconds: float):
     cport.build()
     Q = batch.n_plans
     n = Q
+    cport.map_sweep(batch.desc[:1], batch.plans, batch.alive, batch.tok, cores)  # load / warm
+    probe = np.arange(0, Q, max(1, Q // (4 * cores)))[:4 * cores]
     t0 = time.perf_counter()
-    cport.map_sweep(batch.desc[:1], batch.plans, batch.alive, batch.tok, cores)
-    one = time.perf_counter() - t0
+    cport.map_sweep(batch.desc[probe], batch.plans, batch.alive, batch.tok, cores)
+    one = (time.perf_counter() - t0) * cores / len(probe)  # single-core seconds per plan
     if one * Q / cores > seconds:
         n = max(cores, int(seconds * cores / max(one, 1e-6)))
     step = max(1, Q // n)
