@@ -909,8 +909,8 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       // (at most flips the sign of a zero, which no comparison or later
       // non-zero result can observe), so the update is skipped
       if (delta != 0.0) {
-#pragma unroll
         if (pt == 0) ucol[0] += delta;  // column 0: the current row's u
+#pragma unroll
         for (int k = 0; k < CPL; ++k) {
           const bool u = (used >> k) & 1u;
           if (u) ucol[1 + pt + T * k] += delta;
@@ -1336,8 +1336,10 @@ int sk_sweep_expand(const sk_sweep_desc* d_desc, int n_desc, const uint32_t* d_a
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int p0 = 0; p0 < n_desc; p0 += kMaxGridY) {
     const int np = n_desc - p0 < kMaxGridY ? n_desc - p0 : kMaxGridY;
-    dim3 grid((max_rows + 127) / 128, np);
-    k_sweep_expand<<<grid, 128, 0, s>>>(d_desc + p0, d_alive, d_tok, d_plans, d_row_ptr, d_segs);
+    // 64-row blocks: plans have ~R = 64 k + small rows, so 128-row blocks
+    // would leave up to half of a plan's last block idle
+    dim3 grid((max_rows + 63) / 64, np);
+    k_sweep_expand<<<grid, 64, 0, s>>>(d_desc + p0, d_alive, d_tok, d_plans, d_row_ptr, d_segs);
     int rc = cuda_check("k_sweep_expand launch");
     if (rc) return rc;
   }
