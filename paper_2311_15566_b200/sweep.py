@@ -146,6 +146,9 @@ def cpl_bucket(n: int):
         return (1, need)
     if need <= 8:
         return (1, 8)
+    need2 = (n + 63) // 64
+    if need2 <= 8:
+        return (2, 5 if need2 <= 5 else (6 if need2 <= 6 else 8))
     need4 = (n + 127) // 128
     for c in (3, 4, 5, 6, 8, 12, 16):
         if need4 <= c:
