@@ -540,9 +540,12 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": survey_bytes,
                 "per_unit": "16*R*C bytes per plan (SURVEY.md 8d) x plans per step",
                 "design_bytes_per_launch": kernels[dom]["bytes"],
+                "issue": ncu_traffic(dom + "_issue", wl_key),
                 "note": "W is never materialised (built on the fly inside the inner KM), so "
                         "measured DRAM traffic is below the 16RC figure; the outer KM is a "
-                        "sequential Dijkstra chain per plan (latency-bound), see outer_km"}
+                        "sequential Dijkstra chain per plan bound by instruction issue "
+                        "(`issue`: duration-weighted IPC / issue-active % from the committed "
+                        "ncu capture, peak IPC 4), see outer_km"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": dev_ms_max / K, "higher_is_better": True, "scaling": "weak",
