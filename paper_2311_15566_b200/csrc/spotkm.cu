@@ -4,13 +4,16 @@
 //
 // Kernels
 //   k_weights      K1  dense W[R][C] (build_graph, mapping.py:184-216)
-//   k_fuse<g>      K2a per fused pair: g x g weight block built on the fly,
-//                      inner KM, fused weight (mapping.py:258-269)
-//   k_outer<CPL>   K2b one warp per plan: outer KM on the zero-padded fused
-//                      matrix (mapping.py:271, 71-122) + expansion and
-//                      total_weight in reference order (mapping.py:272-283)
+//   k_fuse<g, lpg> K2a per fused GPU group (one fused row): g x g weight
+//                      blocks built on the fly, inner KM, fused weight
+//                      (mapping.py:258-269)
+//   k_outer<CPL, mode, W>
+//                  K2b W warps per plan: outer KM on the dictionary-coded,
+//                      zero-padded fused matrix (mapping.py:271, 71-122) +
+//                      expansion and total_weight in reference order
+//                      (mapping.py:272-283)
 //   k_sweep_expand     compact sweep descriptors -> rows/segments
-//   k_copy         K3  byte-range copies (peer-mapped pull over NVLink)
+//   k_copy         K3  byte-range copies (peer-mapped push/pull over NVLink)
 //
 // Exactness: no fast-math, -fmad=false.  Every float op of the reference's
 // _hungarian_max is replayed in the same order: cost = -w;
@@ -252,7 +255,7 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
 struct FusedBlock {
   double f;
   uint32_t packed;
-  bool nz;  // false: all-zero block (the pre-cleared buffers already hold it)
+  bool nz;  // false: all-zero block (the row's zero fill already holds it)
 };
 
 // Block of row group a x fused slot decoded by c0, counting the model
@@ -292,7 +295,7 @@ __device__ __forceinline__ FusedBlock fuse_block(const sk_plan& p, int a, const 
   out.nz = any != 0;
   // all-zero block: max / builtin sum of zeros are 0.0 and the inner KM's
   // answer is the (replayed) zero-matrix permutation -- exactly what the
-  // pre-cleared buffers already encode (F = 0.0, perm stored XOR zero_perm)
+  // row's zero fill already encodes (F = 0.0, perm stored XOR zero_perm)
   if (!out.nz) return out;
   // N / K: exact reciprocal multiply when K is a power of two (bit-identical
   // to the correctly rounded division), else the IEEE division
