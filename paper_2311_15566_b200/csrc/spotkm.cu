@@ -738,24 +738,22 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int e = e0 + u * T + pt;
-        // one insert per distinct value per warp: the lowest lane holding it
-        const unsigned peers = __match_any_sync(kFull, bits[u]);
-        const int leader = __ffs(peers) - 1;
-        unsigned h = 0;
-        if (lane == leader && bits[u] != kEmpty) {
-          h = (unsigned)((bits[u] * 0x9E3779B97F4A7C15ull) >> 56);
-          for (int tries = 0;; ++tries) {
-            const unsigned long long old = atomicCAS(table + h, kEmpty, bits[u]);
-            if (old == kEmpty || old == bits[u]) break;
-            h = (h + 1) & (kDictSlots - 1);
-            if (tries + 1 == kDictSlots) {
-              fail = true;
-              break;
-            }
+        if (bits[u] == kEmpty) continue;
+        // open addressing, every thread for itself: a plain shared load finds
+        // values already in the table (almost all of them); only an empty
+        // slot takes a CAS, and racing inserts of one value agree through it
+        unsigned h = (unsigned)((bits[u] * 0x9E3779B97F4A7C15ull) >> 56);
+        for (int tries = 0;; ++tries) {
+          unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(table + h);
+          if (cur == kEmpty) cur = atomicCAS(table + h, kEmpty, bits[u]);
+          if (cur == kEmpty || cur == bits[u]) break;
+          h = (h + 1) & (kDictSlots - 1);
+          if (tries + 1 == kDictSlots) {
+            fail = true;
+            break;
           }
         }
-        h = __shfl_sync(kFull, h, leader);
-        if (bits[u] != kEmpty) codes[e] = (unsigned char)h;
+        codes[e] = (unsigned char)h;
       }
     }
     if (W == 1) {
