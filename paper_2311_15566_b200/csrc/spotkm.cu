@@ -1134,6 +1134,11 @@ int global_codes_threshold() {
 // launch is big enough (>= 2 waves) for the extra concurrency to pay
 int outer_mode(int n_plans, int max_n, int max_rows, int W, int CPL, bool have_codes) {
   constexpr int kSMs = 148;
+  static const bool force_global = [] {  // testing: every class with a scratch
+    const char* e = getenv("SK_OUTER_FORCE_GLOBAL");
+    return e && atoi(e) != 0;
+  }();
+  if (have_codes && force_global) return kOuterGlobalCodes;
   int res = 0;
   best_per_block(outer_smem_per_warp(max_n, max_rows, kOuterSmemCodes, W, CPL), W, kSmemCodedCap, &res);
   const bool few = res < global_codes_threshold() && (long long)n_plans > 2LL * kSMs * res;

@@ -92,3 +92,32 @@ def test_global_code_mode_matches_c_oracle():
     exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
     assert np.array_equal(assign, exp_assign)
     assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
+
+
+@pytest.mark.parametrize("n_pos", [128, 512])
+def test_forced_global_codes_all_shapes_match_c_oracle(n_pos):
+    """Every size class (1-, 2- and 4-warp shapes) in the global-code mode,
+    forced with SK_OUTER_FORCE_GLOBAL in a subprocess (the mode is chosen per
+    launch from the class size, so small test batches would not reach it)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from oracle import cport\n"
+        "from paper_2311_15566_b200 import sweep\n"
+        f"b = sweep.make_sweep({n_pos}, 2, seed=41)\n"
+        "r = sweep.SweepRunner(b)\n"
+        "assert all(x > 0 for x in r.codes_need), r.codes_need\n"
+        "assign, totals = r.run()\n"
+        "ea, et = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)\n"
+        "assert np.array_equal(assign, ea)\n"
+        "assert [t.hex() for t in totals] == [t.hex() for t in et]\n"
+        "print('ok', b.n_plans)\n")
+    env = dict(os.environ, SK_OUTER_FORCE_GLOBAL="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    assert res.stdout.startswith("ok")
