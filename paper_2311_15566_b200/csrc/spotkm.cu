@@ -1184,11 +1184,9 @@ void outer_shape(int max_n, int* cpl, int* w) {
 
 template <int CPL, int MODE, int W>
 void configure_outer() {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(k_outer<CPL, MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    done = true;
-  }
+  // per launch (a few microseconds): the attribute belongs to the current
+  // device's context, and callers may switch devices between launches
+  cudaFuncSetAttribute(k_outer<CPL, MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 template <int CPL, int W>
