@@ -267,8 +267,8 @@ def run_reference(args):
     return 0
 
 
-# preemption sets per chunk for the all-sizes sweep (device scratch <= ~45 GB)
-SIZE_CHUNK_SETS = {64: 4096, 128: 4096, 256: 4096, 512: 2048, 1024: 1024}
+# preemption sets per chunk for the all-sizes sweep (device scratch <= ~90 GB)
+SIZE_CHUNK_SETS = {64: 4096, 128: 4096, 256: 4096, 512: 4096, 1024: 2048}
 
 
 class Chunked:
