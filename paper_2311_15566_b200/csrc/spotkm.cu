@@ -732,7 +732,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         r = c < 0 ? r - 1 : (c >= n ? r + 1 : r);
         c = c < 0 ? c + n : (c >= n ? c - n : c);
         const bool in = e < cnt && r < nA && c < nB;
-        const unsigned long long x = (unsigned long long)__double_as_longlong(__ldg(Fp + (in ? r * nB + c : 0)));
+        const unsigned long long x = (unsigned long long)__double_as_longlong(__ldcs(Fp + (in ? r * nB + c : 0)));
         bits[u] = in ? x : (e < cnt ? 0ull : kEmpty);
       }
 #pragma unroll
