@@ -368,7 +368,13 @@ __device__ __forceinline__ FusedBlock fuse_block(const sk_plan& p, int a, const 
 // does not name -- and the full block of each (named pipeline, offset): the
 // same numbers give the same inner KM, so the reuse is exact, and a group
 // builds span * (1 + named pipelines) blocks instead of D * span.
-constexpr int kF_TPB = 128;
+// 3 warps per CTA: at 112 registers a warp takes 3.5 K registers, so the SM
+// holds 18 warps as six 3-warp CTAs but only 16 as four 4-warp CTAs
+// (measured: k_fuse 8.70 -> 8.50 ms per step; 32/64/128/160/192/256 slower)
+#ifndef SK_F_TPB
+#define SK_F_TPB 96
+#endif
+constexpr int kF_TPB = SK_F_TPB;
 constexpr int kF_WARPS = kF_TPB / 32;
 constexpr int kF_MAXD = 128;  // pipelines tracked by the cache-pipeline mask
 
