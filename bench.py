@@ -412,6 +412,7 @@ def _reshard_once(world, rank, K, W, mode, nccl_baseline, case):
     ex = reshard.ReshardExecutor(plan, layout, need, model, owner, rank, world, mode=mode)
     ex.fill_old()
     torch.cuda.synchronize()
+    dist.barrier()   # every peer's old slab is filled before anyone pulls from it
     bin_, bout = reshard.traffic(plan)
     peak_gpu = max(max(bin_.values(), default=0), max(bout.values(), default=0))
     for _ in range(W):

@@ -294,6 +294,23 @@ typedef struct sk_timeline_input {
 
 int sk_plan_timeline(const sk_timeline_input* t, double* ends);
 
+/* migration_cost (costmodel.py:231-260) on the host: the timeline above, then
+ * the full duration, or with progressive != 0 the worst stage-ready
+ * constraint; act_stage[a] = stage of a start_stage action, else -1;
+ * step = t_dec(config) / P (0 without a config). */
+int sk_migration_cost(const sk_timeline_input* t, const int32_t* act_stage, double step,
+                      int32_t progressive, double* cost);
+
+/* simulate_buffer_usage (migration.py:387-401): per-instance peak bytes of a
+ * plan replay.  Instances 0..n_seed-1 are the old layout's, in its order;
+ * per action a: received transfers tr_ptr[a]..tr_ptr[a+1] (dst instance,
+ * bytes) then end-of-round releases rel_ptr[a]..; name_rank orders
+ * instances by id string.  order[0..*n_order) = the result's key order. */
+int sk_simulate_buffer_usage(int32_t n_inst, int32_t n_seed, int32_t n_actions, const int32_t* tr_ptr,
+                             const int32_t* tr_dst, const double* tr_bytes, const int32_t* rel_ptr,
+                             const int32_t* rel_inst, const double* rel_bytes, const int32_t* name_rank,
+                             double* peaks, int32_t* order, int32_t* n_order);
+
 /* Batched migration_cost (costmodel.py:231-260 over plan_timeline 189-228)
  * for many candidate plans on the device, one thread per plan.  Per plan:
  * actions [act_begin, act_end) (CSR act_ptr into the transfer arrays;

@@ -44,7 +44,8 @@ EXPORTS = (
     "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
     "sk_ipc_open_handle", "sk_ipc_close_handle", "sk_fill_regions", "sk_verify_regions",
-    "sk_reshard_error", "sk_migration_cost_batched",
+    "sk_reshard_error", "sk_migration_cost_batched", "sk_migration_cost",
+    "sk_simulate_buffer_usage",
 )
 
 

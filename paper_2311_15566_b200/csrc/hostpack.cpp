@@ -178,7 +178,9 @@ bool load_need(PyObject* need, NeedMap* out) {
         Py_DECREF(seq);
         return false;
       }
-      v.emplace_back((int32_t)dv, tv);
+      // pipeline 0 would read as a model segment; callers filter the range
+      // 1..D (pack.need_tokens), this keeps the encoding sound regardless
+      if (dv >= 1 && dv <= 0x7fffffffLL) v.emplace_back((int32_t)dv, tv);
     }
     Py_DECREF(seq);
   }

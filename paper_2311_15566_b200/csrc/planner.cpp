@@ -696,6 +696,77 @@ int sk_plan_timeline(const sk_timeline_input* t, double* ends) {
   return SK_OK;
 }
 
+// migration_cost (costmodel.py:231-260): the timeline above, then the full
+// duration or, with progressive start, the worst stage-ready constraint over
+// the start_stage actions taken in stable stage order
+int sk_migration_cost(const sk_timeline_input* t, const int32_t* act_stage, double step, int32_t progressive,
+                      double* cost) {
+  std::vector<double> ends(t->n_actions > 0 ? t->n_actions : 1, 0.0);
+  sk_plan_timeline(t, ends.data());
+  const double last = t->n_actions > 0 ? ends[t->n_actions - 1] : t->start;
+  const double total = (last > t->start ? last : t->start) - t->start;
+  std::vector<std::pair<int32_t, double>> starts;
+  if (progressive)
+    for (int a = 0; a < t->n_actions; ++a)
+      if (act_stage[a] >= 0) starts.push_back({act_stage[a], ends[a]});
+  if (starts.empty()) {
+    *cost = total;
+    return SK_OK;
+  }
+  std::stable_sort(starts.begin(), starts.end(),
+                   [](const std::pair<int32_t, double>& x, const std::pair<int32_t, double>& y) {
+                     return x.first < y.first;
+                   });
+  double stall = 0.0;
+  for (size_t o = 0; o < starts.size(); ++o) {
+    const double v = starts[o].second - t->start - (double)o * step;
+    if (v > stall) stall = v;  // max(stall, v): the first maximum is kept
+  }
+  *cost = stall > 0.0 ? stall : 0.0;
+  return SK_OK;
+}
+
+// simulate_buffer_usage (migration.py:387-401): per-instance usage replay.
+// Instances 0..n_seed-1 are the old layout's (in its order); `order` receives
+// the instances in the result dict's insertion order, *n_order their count.
+int sk_simulate_buffer_usage(int32_t n_inst, int32_t n_seed, int32_t n_actions, const int32_t* tr_ptr,
+                             const int32_t* tr_dst, const double* tr_bytes, const int32_t* rel_ptr,
+                             const int32_t* rel_inst, const double* rel_bytes, const int32_t* name_rank,
+                             double* peaks, int32_t* order, int32_t* n_order) {
+  std::vector<double> usage(n_inst, 0.0);
+  std::vector<char> in_peaks(n_inst, 0);
+  int32_t no = 0;
+  for (int i = 0; i < n_seed; ++i) {
+    peaks[i] = 0.0;
+    in_peaks[i] = 1;
+    order[no++] = i;
+  }
+  for (int a = 0; a < n_actions; ++a) {
+    std::vector<int32_t> touched;
+    for (int k = tr_ptr[a]; k < tr_ptr[a + 1]; ++k) {
+      usage[tr_dst[k]] = usage[tr_dst[k]] + tr_bytes[k];
+      touched.push_back(tr_dst[k]);
+    }
+    // sorted({t.dst[0] ...}): by instance name (name_rank = rank of the string)
+    std::sort(touched.begin(), touched.end(),
+              [&](int32_t x, int32_t y) { return name_rank[x] < name_rank[y]; });
+    touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
+    for (int32_t i : touched) {
+      if (!in_peaks[i]) {
+        in_peaks[i] = 1;
+        peaks[i] = usage[i];  // max(peaks.get(inst, 0.0), usage) with 0.0 first
+        if (!(usage[i] > 0.0)) peaks[i] = 0.0;
+        order[no++] = i;
+      } else if (usage[i] > peaks[i]) {
+        peaks[i] = usage[i];
+      }
+    }
+    for (int k = rel_ptr[a]; k < rel_ptr[a + 1]; ++k) usage[rel_inst[k]] = usage[rel_inst[k]] - rel_bytes[k];
+  }
+  *n_order = no;
+  return SK_OK;
+}
+
 int sk_memopt_order(int32_t n_layers, int32_t n_inst, const int32_t* in_ptr, const int32_t* in_inst,
                     const double* in_bytes, const int32_t* fr_ptr, const int32_t* fr_inst,
                     const double* fr_bytes, int32_t has_umax, double u_max, int32_t* order) {

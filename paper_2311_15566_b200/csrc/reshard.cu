@@ -148,11 +148,11 @@ __global__ void k_migration_cost(const sk_tl_plan* __restrict__ plans, int n_pla
   }
   const double start = p.start;
   double prev = start;
-  // progressive bookkeeping: (stage, ready) of start_stage actions, sorted by stage
-  constexpr int kMaxStages = 64;
-  int st_stage[kMaxStages];
-  double st_ready[kMaxStages];
-  int n_st = 0;
+  // progressive start: each start_stage action's rank in the stable sort by
+  // stage is counted from the (static) stage list, so no per-plan array
+  // bounds the number of stages
+  double stall = 0.0;
+  bool any_start = false;
   for (int a = p.act_begin; a < p.act_end; ++a) {
     double end = prev;
     bool moved = false;
@@ -174,29 +174,24 @@ __global__ void k_migration_cost(const sk_tl_plan* __restrict__ plans, int n_pla
     if (moved) end += latency;
     const double e = end > prev ? end : prev;
     prev = e;
-    if (act_stage[a] >= 0 && n_st < kMaxStages) {
-      // insertion by stage keeps the stable sort of sorted(starts, key=stage)
-      int pos = n_st;
-      while (pos > 0 && st_stage[pos - 1] > act_stage[a]) {
-        st_stage[pos] = st_stage[pos - 1];
-        st_ready[pos] = st_ready[pos - 1];
-        --pos;
+    const int st = act_stage[a];
+    if (p.progressive && st >= 0) {
+      int o = 0;  // entries before this one in sorted(starts, key=stage)
+      for (int b = p.act_begin; b < p.act_end; ++b) {
+        const int sb = act_stage[b];
+        if (sb >= 0 && (sb < st || (sb == st && b < a))) ++o;
       }
-      st_stage[pos] = act_stage[a];
-      st_ready[pos] = e;
-      ++n_st;
+      // max(stall, x) over the sorted order: the value is order-independent
+      const double x = e - start - (double)o * p.step;
+      if (x > stall) stall = x;
+      any_start = true;
     }
   }
   const double last = p.act_end > p.act_begin ? prev : start;
   const double total = (last > start ? last : start) - start;
-  if (!p.progressive || n_st == 0) {
+  if (!p.progressive || !any_start) {
     cost[q] = total;
     return;
-  }
-  double stall = 0.0;
-  for (int o = 0; o < n_st; ++o) {
-    const double x = st_ready[o] - start - (double)o * p.step;
-    if (x > stall) stall = x;
   }
   cost[q] = stall > 0.0 ? stall : 0.0;
 }

@@ -407,7 +407,9 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
       if (sg.l1 > sg.l0 && sg.b > sg.a && sg.unit != 0) {
         lo = min(lo, sg.l0);
         hi = max(hi, sg.l1);
-        if (sg.pipe != 0) {
+        // cache segments of pipelines outside 1..D match no column
+        // (seg_num compares pipe with the column's d <= D): not named
+        if (sg.pipe != 0 && sg.pipe <= p.D) {
           const int q = sg.pipe - 1;
           if (q < 64)
             pm0 |= 1ull << q;
@@ -490,7 +492,8 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
       perm[row0 + bq] = pk;
     } else {
       for (int d = 0; d < p.D; ++d) {
-        if ((d < 64 ? pm0 >> d : pm1 >> (d - 64)) & 1ull) continue;
+        const bool named = d < 64 ? ((pm0 >> d) & 1ull) : d < kF_MAXD ? ((pm1 >> (d - 64)) & 1ull) : false;
+        if (named) continue;
         const int b = d * per_d + b0 + o;
         F[row0 + b] = r.f;
         perm[row0 + b] = pk;

@@ -103,7 +103,7 @@ def _pack_problem(instances, target, model, inheritance, requests_by_old_pipelin
     prob.rows = len(refs)
     prob.D, prob.P, prob.M = target.data_parallel, target.pipeline_stages, target.tensor_shards
     prob.L = model.num_layers
-    need = need_tokens(inherited_by_new(inheritance, requests_by_old_pipeline))
+    need = need_tokens(inherited_by_new(inheritance, requests_by_old_pipeline), prob.D)
     try:
         prob.K = common_denominator(invs, prob.M)
         prob.row_ptr, prob.segs = pack_rows(invs, prob.K, model.bytes_per_layer,

@@ -81,11 +81,15 @@ def inherited_by_new(inheritance, requests_by_old_pipeline):
     return out
 
 
-def need_tokens(inherited: dict) -> dict:
+def need_tokens(inherited: dict, n_pipelines: int | None = None) -> dict:
     """rid -> [(new pipeline, tokens)] for tokens > 0 (the filter of
-    mapping.py:167)."""
+    mapping.py:167).  Only new pipelines 1..n_pipelines have positions
+    (build_graph looks entries up by pos.pipeline, mapping.py:210-213), so an
+    inheritance target outside that range contributes nothing and is dropped."""
     out: dict[str, list] = {}
     for d_new in sorted(inherited):
+        if n_pipelines is not None and not 1 <= d_new <= n_pipelines:
+            continue
         for rid, tok in inherited[d_new]:
             if tok > 0:
                 out.setdefault(rid, []).append((d_new, tok))

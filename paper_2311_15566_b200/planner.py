@@ -80,6 +80,10 @@ def _lib():
         lib.sk_plan_timeline.restype = i32
         lib.sk_memopt_order.argtypes = [i32, i32, vp, vp, vp, vp, vp, vp, i32, dbl, vp]
         lib.sk_memopt_order.restype = i32
+        lib.sk_migration_cost.argtypes = [vp, vp, dbl, i32, vp]
+        lib.sk_migration_cost.restype = i32
+        lib.sk_simulate_buffer_usage.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.sk_simulate_buffer_usage.restype = i32
         lib.sk_rat_to_double.argtypes = [i64, ctypes.c_uint64, i64]
         lib.sk_rat_to_double.restype = dbl
         lib._planner_sigs = True
@@ -295,23 +299,41 @@ def memopt_layer_order(traffic_by_layer, u_max):
 
 def simulate_buffer_usage(plan, old_layout) -> dict:
     """(reference: migration.py:387-401): replay receives and end-of-round
-    releases; per-instance peak.  Pure bookkeeping over the plan's floats."""
-    usage: dict = {}
+    releases; per-instance peak -- computed by sk_simulate_buffer_usage."""
+    names: dict = {}
     for gpu in old_layout:
-        usage.setdefault(gpu[0], 0.0)
-    peaks = dict(usage)
+        names.setdefault(gpu[0], len(names))
+    n_seed = len(names)
+    tr_ptr, tr_dst, tr_b, rel_ptr, rel_i, rel_b = [0], [], [], [0], [], []
     for action in plan.actions:
         for tr in action.transfers:
-            usage[tr.dst[0]] = usage.get(tr.dst[0], 0.0) + tr.bytes
-        for inst in sorted({t.dst[0] for t in action.transfers}):
-            peaks[inst] = max(peaks.get(inst, 0.0), usage[inst])
+            tr_dst.append(names.setdefault(tr.dst[0], len(names)))
+            tr_b.append(tr.bytes)
         for inst, b in action.releases:
-            usage[inst] = usage.get(inst, 0.0) - b
-    return peaks
+            rel_i.append(names.setdefault(inst, len(names)))
+            rel_b.append(b)
+        tr_ptr.append(len(tr_dst))
+        rel_ptr.append(len(rel_i))
+    n = max(len(names), 1)
+    by_name = sorted(names, key=lambda x: x)
+    rank = np.zeros(n, dtype=np.int32)
+    for r, name in enumerate(by_name):
+        rank[names[name]] = r
+    arrs = [np.array(tr_ptr, np.int32), np.array(tr_dst or [0], np.int32),
+            np.array(tr_b or [0.0], np.float64), np.array(rel_ptr, np.int32),
+            np.array(rel_i or [0], np.int32), np.array(rel_b or [0.0], np.float64)]
+    peaks = np.zeros(n, dtype=np.float64)
+    order = np.zeros(n, dtype=np.int32)
+    n_order = ctypes.c_int32(0)
+    _lib().sk_simulate_buffer_usage(len(names), n_seed, len(plan.actions), *(_p(a) for a in arrs),
+                                    _p(rank), _p(peaks), _p(order), ctypes.addressof(n_order))
+    inv = {i: name for name, i in names.items()}
+    return {inv[int(i)]: float(peaks[int(i)]) for i in order[:n_order.value]}
 
 
-def plan_timeline(plan, profile, release=None, start=0.0) -> list:
-    """(reference: costmodel.py:189-228), computed by sk_plan_timeline."""
+def _timeline_input(plan, profile, release, start):
+    """Flatten a plan for sk_plan_timeline / sk_migration_cost.  Returns the
+    struct and the arrays it points into (kept alive by the caller)."""
     release = release or {}
     names: dict = {}
     ptr, src, dst, byt = [0], [], [], []
@@ -330,12 +352,18 @@ def plan_timeline(plan, profile, release=None, start=0.0) -> list:
         has_rel[names[name]] = 1
         rel[names[name]] = float(t)
     arrs = [np.array(ptr, np.int32), np.array(src or [0], np.int32), np.array(dst or [0], np.int32),
-            np.array(byt or [0.0], np.float64)]
+            np.array(byt or [0.0], np.float64), has_rel, rel]
     ti = _TimelineInput()
     ti.n_inst, ti.n_actions = n, len(plan.actions)
-    ti.action_ptr, ti.src_inst, ti.dst_inst, ti.bytes = (_p(a) for a in arrs)
+    ti.action_ptr, ti.src_inst, ti.dst_inst, ti.bytes = (_p(a) for a in arrs[:4])
     ti.bandwidth, ti.latency, ti.start = float(profile.bandwidth), float(profile.transfer_latency), float(start)
     ti.has_release, ti.release = _p(has_rel), _p(rel)
+    return ti, arrs
+
+
+def plan_timeline(plan, profile, release=None, start=0.0) -> list:
+    """(reference: costmodel.py:189-228), computed by sk_plan_timeline."""
+    ti, _keep = _timeline_input(plan, profile, release, start)
     ends = np.zeros(max(len(plan.actions), 1), dtype=np.float64)
     _lib().sk_plan_timeline(ctypes.byref(ti), _p(ends))
     return ends[:len(plan.actions)].tolist()
@@ -343,19 +371,16 @@ def plan_timeline(plan, profile, release=None, start=0.0) -> list:
 
 def migration_cost(plan, profile, config=None, progressive=False, release=None, start=0.0) -> float:
     """(reference: costmodel.py:231-260): full T_mig, or with progressive start
-    the worst stage-ready constraint."""
-    timeline = plan_timeline(plan, profile, release=release, start=start)
-    total = max(timeline[-1] if timeline else start, start) - start
-    if not progressive:
-        return total
-    starts = [(a.stage, end) for a, end in zip(plan.actions, timeline) if a.kind == "start_stage"]
-    if not starts:
-        return total
-    step = profile.decode_seconds(config) / config.pipeline_stages if config is not None else 0.0
-    stall = 0.0
-    for order, (_stage, ready) in enumerate(sorted(starts, key=lambda s: s[0])):
-        stall = max(stall, ready - start - order * step)
-    return max(0.0, stall)
+    the worst stage-ready constraint -- computed by sk_migration_cost."""
+    ti, _keep = _timeline_input(plan, profile, release, start)
+    stages = np.array([a.stage if a.kind == "start_stage" else -1 for a in plan.actions] or [-1],
+                      dtype=np.int32)
+    step = 0.0
+    if progressive and config is not None:
+        step = profile.decode_seconds(config) / config.pipeline_stages
+    out = np.zeros(1, dtype=np.float64)
+    _lib().sk_migration_cost(ctypes.byref(ti), _p(stages), float(step), 1 if progressive else 0, _p(out))
+    return float(out[0])
 
 
 def plan_to_dict(plan) -> dict:
@@ -446,7 +471,7 @@ def migration_cost_many(plans, profile, configs=None, progressive=False, release
         has_rel += flags
         rel += vals
         cfg = configs[q]
-        step = profile.decode_seconds(cfg) / cfg.pipeline_stages if cfg is not None else 0.0
+        step = profile.decode_seconds(cfg) / cfg.pipeline_stages if (progressive and cfg is not None) else 0.0
         tl[q] = (n_act, n_act + len(plan.actions), inst_base, len(names), float(starts[q]), step,
                  1 if progressive else 0, 0)
         n_act += len(plan.actions)

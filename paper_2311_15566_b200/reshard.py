@@ -369,11 +369,19 @@ class ReshardExecutor:
                                                  torch.cuda.current_stream().cuda_stream))
         return int(self.d_bad.item())
 
-    def close(self):
+    def close(self, group=None):
+        """Unmap the peers' slabs, then free this rank's own.  With world > 1
+        every rank must have unmapped a slab before its owner frees it
+        (cudaIpcCloseMemHandle before cudaFree), so a barrier separates the
+        two halves; all ranks must call close()."""
         torch.cuda.synchronize()
         for p in self.opened:
             self.lib.sk_ipc_close_handle(p)
         self.opened = []
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.barrier(group=group)
         for m in list(self.old_mem.values()) + list(self.new_mem.values()):
             m.free()
 

@@ -16,3 +16,13 @@ from paper_2311_15566_b200.install import install
 PARTS = tuple(os.environ.get("SPOTKM_INSTALL_PARTS", "planner,estimator").split(","))
 REPLACED = install(spotsim, parts=PARTS)
 assert REPLACED, "nothing was rebound"
+
+if "mapper" in PARTS:
+    # the device mapper has no CPU fallback: make sure the CUDA library is the
+    # thing these tests exercise
+    import torch
+
+    from paper_2311_15566_b200 import _native
+
+    assert torch.cuda.is_available(), "mapper drop-in needs a GPU"
+    _native.load()
