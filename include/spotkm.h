@@ -35,13 +35,13 @@
 extern "C" {
 #endif
 
-#define SPOTKM_ABI_VERSION 1
+#define SPOTKM_ABI_VERSION 2
 
 typedef enum {
   SK_OK = 0,
   SK_EINVAL = 1,    /* malformed arguments                       -> MappingError   */
   SK_EGROUP = 2,    /* fused group does not divide G and M        -> MappingError   */
-  SK_ERANGE = 3,    /* numerator bound >= 2^53 (inexact)          -> MappingError   */
+  SK_ERANGE = 3,    /* numerator bound >= 2^127 / K >= 2^62       -> MappingError   */
   SK_ENOSOURCE = 4, /* a required shard has no live holder        -> MigrationError */
   SK_ECUDA = 5,     /* CUDA runtime error                         -> RuntimeError   */
   SK_ENOPEER = 6    /* peer access unavailable for the executor   -> RuntimeError   */
@@ -50,6 +50,8 @@ typedef enum {
 /* plan flags */
 #define SK_PLAN_FUSED_SUM 1 /* fused edge weight = Python builtin sum() of the inner match (else max) */
 #define SK_PLAN_DENSE 2     /* the F buffer holds a caller-given dense W (km_match); no segments      */
+#define SK_PLAN_GENERIC 4   /* general-range plan: wide segments (sk_segment_wide), 128-bit
+                               numerators, 64-bit K, any fused group 1..32 (see sk_map_fuse)     */
 
 /*
  * One context segment of an old GPU's inventory: layers [l0, l1) x the
@@ -70,6 +72,21 @@ typedef struct sk_segment {
 } sk_segment; /* 32 bytes */
 
 /*
+ * The same segment for SK_PLAN_GENERIC plans, whose endpoints may exceed
+ * int32 (K up to 2^62) and whose numerators may exceed 2^53 (accumulated in
+ * 128 bits; every plan's sum_seg (l1-l0)(b-a)unit < 2^127, checked on the
+ * host).  It occupies TWO sk_segment slots; row_ptr counts slots.
+ */
+typedef struct sk_segment_wide {
+  int32_t l0, l1;
+  int32_t pipe;
+  int32_t reserved;
+  int64_t a, b;
+  int64_t unit;
+  int64_t reserved2[3];
+} sk_segment_wide; /* 64 bytes = 2 x sk_segment */
+
+/*
  * One mapping problem (one build_graph / map_devices call).
  * Rows are the candidate GPUs in the reference row order (instances by
  * natural_key, then local index; mapping.py:193-198); columns are the target
@@ -79,15 +96,23 @@ typedef struct sk_plan {
   int32_t rows;     /* R = candidate GPUs                                       */
   int32_t D, P, M;  /* target configuration                                     */
   int32_t L;        /* model layers                                             */
-  int32_t K;        /* common denominator of every interval (multiple of M)     */
+  int32_t K;        /* common denominator of every interval (multiple of M), <= 2^31-1;
+                       0 for SK_PLAN_GENERIC plans, which carry it in Kw        */
   int32_t group;    /* fused group size g = min(G, M) (1 = flat km_match)       */
   int32_t flags;    /* SK_PLAN_*                                                */
   int32_t row_base; /* row r's segments: seg[row_ptr[row_base+r] .. row_ptr[row_base+r+1]) */
   int32_t reserved;
-  int64_t f_off;    /* element offset of the plan's fused matrix (nA x nB) and perm block */
+  int64_t f_off;    /* element offset of the plan's fused matrix (nA x nB) and perm block;
+                       SK_PLAN_GENERIC plans use sk_fused_elems() doubles there  */
   int64_t out_off;  /* element offset of the plan's R assignment entries        */
-  int64_t reserved2;
+  int64_t Kw;       /* SK_PLAN_GENERIC: the common denominator, < 2^62          */
 } sk_plan; /* 64 bytes */
+
+/* Elements of the fused buffer one plan occupies at f_off: nA*nB for the
+ * regular path; for SK_PLAN_GENERIC plans the fused matrix is followed by
+ * the g matched weights and the g inner-permutation bytes of every fused
+ * pair: nA*nB*(1+g) doubles + ceil(nA*nB*g / 8). */
+int64_t sk_fused_elems(int32_t nA, int32_t nB, int32_t group, int32_t flags);
 
 /* Library / ABI identification. */
 int sk_abi_version(void);
@@ -100,6 +125,8 @@ const char* sk_last_error(void);
 int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
                      const sk_segment* d_segs, double* d_W, int max_rows, int max_cols,
                      void* stream);
+/* (SK_PLAN_GENERIC plans: 128-bit numerators, one correctly rounded
+ * conversion each -- the same float(Fraction) value for any size.) */
 
 /*
  * K2 -- map_devices (mapping.py:222-283) for a batch of plans: per fused pair
@@ -112,7 +139,10 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
  *   d_assign: per plan R int32 at out_off: column index or -1 (unassigned)
  *   d_total : per plan total_weight (accumulated in the reference order)
  *   max_na / max_nb = max fused rows / slots (R/g, C/g), max_rows = max R over the batch.
- *   group_mask: bit g set when some plan has group g (0 = any of 1..8).
+ *   group_mask: bit g set when some plan has group g (1..8), bit 0 when some
+ *               plan is SK_PLAN_GENERIC (0 = launch everything).
+ *   SK_PLAN_GENERIC plans (any group 1..32, 128-bit numerators): one warp per
+ *   fused pair runs the inner KM on the g x g block in shared memory.
  *   fused_elems: elements of d_fused / d_perm in use (cleared first).
  */
 int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
@@ -148,6 +178,9 @@ int sk_map_outer_codes(const sk_plan* d_plans, int n_plans, const int32_t* d_row
                        int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
                        uint8_t* d_codes, int64_t codes_bytes, void* stream);
 int64_t sk_outer_codes_bytes(int n_plans, int max_n, int max_rows);
+/* Outer problems with n > 4095 (any size) run one 1024-thread CTA per plan
+ * with the column state in device scratch that the call allocates
+ * stream-ordered (cudaMallocAsync) and frees on the same stream. */
 
 /*
  * km_match on caller-given dense weights (mapping.py:125-149): plans with

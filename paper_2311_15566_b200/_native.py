@@ -19,14 +19,19 @@ LIB_PATH = LIB_DIR / "libspotkm.so"
 SK_OK, SK_EINVAL, SK_EGROUP, SK_ERANGE, SK_ENOSOURCE, SK_ECUDA, SK_ENOPEER = range(7)
 SK_PLAN_FUSED_SUM = 1
 SK_PLAN_DENSE = 2
-ABI_VERSION = 1
+SK_PLAN_GENERIC = 4
+ABI_VERSION = 2
+MAX_GENERIC_GROUP = 32   # k_fuse_generic: one warp per fused pair
 
 # numpy mirrors of the C structs (field order and sizes must match spotkm.h)
 SEGMENT = np.dtype([("l0", "<i4"), ("l1", "<i4"), ("a", "<i4"), ("b", "<i4"), ("pipe", "<i4"),
                     ("reserved", "<i4"), ("unit", "<i8")], align=True)
+SEGMENT_WIDE = np.dtype([("l0", "<i4"), ("l1", "<i4"), ("pipe", "<i4"), ("reserved", "<i4"),
+                         ("a", "<i8"), ("b", "<i8"), ("unit", "<i8"), ("reserved2", "<i8", (3,))],
+                        align=True)
 PLAN = np.dtype([("rows", "<i4"), ("D", "<i4"), ("P", "<i4"), ("M", "<i4"), ("L", "<i4"),
                  ("K", "<i4"), ("group", "<i4"), ("flags", "<i4"), ("row_base", "<i4"),
-                 ("reserved", "<i4"), ("f_off", "<i8"), ("out_off", "<i8"), ("reserved2", "<i8")],
+                 ("reserved", "<i4"), ("f_off", "<i8"), ("out_off", "<i8"), ("Kw", "<i8")],
                 align=True)
 SWEEP_DESC = np.dtype([("oD", "<i4"), ("oP", "<i4"), ("oM", "<i4"), ("G", "<i4"), ("n_inst", "<i4"),
                        ("alive_off", "<i4"), ("tok_off", "<i4"), ("plan", "<i4"), ("bpl", "<i8"),
@@ -35,6 +40,7 @@ COPY = np.dtype([("src", "<u8"), ("dst", "<u8"), ("bytes", "<u8")], align=True)
 REGION = np.dtype([("ptr", "<u8"), ("bytes", "<u8"), ("key", "<u8"), ("base", "<u8")])
 TL_PLAN = np.dtype([("act_begin", "<i4"), ("act_end", "<i4"), ("inst_base", "<i4"), ("n_inst", "<i4"),
                     ("start", "<f8"), ("step", "<f8"), ("progressive", "<i4"), ("reserved", "<i4")])
+assert SEGMENT_WIDE.itemsize == 64
 assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize == 48 and COPY.itemsize == 24
 
 EXPORTS = (
@@ -45,7 +51,7 @@ EXPORTS = (
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
     "sk_ipc_open_handle", "sk_ipc_close_handle", "sk_fill_regions", "sk_verify_regions",
     "sk_reshard_error", "sk_migration_cost_batched", "sk_migration_cost",
-    "sk_simulate_buffer_usage",
+    "sk_simulate_buffer_usage", "sk_fused_elems",
 )
 
 
@@ -82,6 +88,7 @@ def load():
         "sk_map_outer_codes": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i64, vp], i32),
         "sk_outer_codes_bytes": ([i32, i32, i32], i64),
         "sk_km_dense": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
+        "sk_fused_elems": ([i32, i32, i32, i32], i64),
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),
         "sk_copy_batched": ([vp, i32, i32, vp], i32),
         "sk_enable_peer_access": ([i32, vp, i32], i32),

@@ -4,7 +4,7 @@
 // Python-level loop per shard.
 //
 //   common_denominator(invs, M)                 -> K
-//   pack_rows(invs, K, bpl, kv, need)           -> (row_ptr bytes, segments bytes)
+//   pack_rows(invs, K, bpl, kv, need[, wide])   -> (row_ptr bytes, segments bytes, wide)
 //       the segment encoding of pack.py (closed form of overlap_bytes,
 //       domain.py:299-320, on required_context_with_cache, mapping.py:155-169)
 //   flatten(invs, K, rid_index, rid_names)      -> (model_ptr, model_shards, cache_ptr, cache_shards)
@@ -12,7 +12,9 @@
 //       into rid_index / rid_names)
 //
 // Exactness: all interval endpoints become integer numerators over K; the
-// numerator bound (< 2^53) is checked exactly with 128-bit integers.
+// numerator bound is checked exactly with 128-bit integers: < 2^53 (and
+// K <= 2^31 - 1) keeps the regular sk_segment encoding, anything below 2^127
+// (K < 2^62) is emitted as sk_segment_wide for the general-range kernels.
 
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
@@ -43,6 +45,23 @@ struct Seg {
   int64_t unit;
 };
 static_assert(sizeof(Seg) == 32, "sk_segment layout");
+
+// sk_segment_wide (include/spotkm.h): two sk_segment slots
+struct WideSeg {
+  int32_t l0, l1, pipe, reserved;
+  int64_t a, b, unit;
+  int64_t reserved2[3];
+};
+static_assert(sizeof(WideSeg) == 64, "sk_segment_wide layout");
+
+// a segment while packing: 64-bit endpoints and units
+struct RunSeg {
+  int32_t l0, l1, pipe;
+  int64_t a, b, unit;
+};
+
+const int64_t kKMax = (int64_t)1 << 62;   // general-range plans: K < 2^62
+const int64_t kKRegular = 0x7fffffffLL;   // regular plans: K <= 2^31 - 1
 
 PyObject* g_num = nullptr;  // interned "numerator"
 PyObject* g_den = nullptr;  // interned "denominator"
@@ -136,13 +155,14 @@ PyObject* py_common_denominator(PyObject*, PyObject* args) {
             Py_DECREF(seq);
             return nullptr;
           }
-          K = std::lcm(K, de);
-          if (K > 0x7fffffffLL) {
+          const i128 l = (i128)(K / std::gcd(K, de)) * de;
+          if (de <= 0 || l >= (i128)kKMax) {
             Py_DECREF(sh);
             Py_DECREF(seq);
-            PyErr_SetString(PyExc_ValueError, "common interval denominator exceeds 2^31-1");
+            PyErr_SetString(PyExc_ValueError, "common interval denominator exceeds 2^62");
             return nullptr;
           }
+          K = (int64_t)l;
         }
       }
       Py_DECREF(sh);
@@ -190,7 +210,8 @@ bool load_need(PyObject* need, NeedMap* out) {
 PyObject* py_pack_rows(PyObject*, PyObject* args) {
   PyObject *invs, *need_obj;
   long long K, bpl, kv;
-  if (!PyArg_ParseTuple(args, "OLLLO", &invs, &K, &bpl, &kv, &need_obj)) return nullptr;
+  int force_wide = 0;
+  if (!PyArg_ParseTuple(args, "OLLLO|p", &invs, &K, &bpl, &kv, &need_obj, &force_wide)) return nullptr;
   NeedMap need;
   if (!load_need(need_obj, &need)) return nullptr;
   PyObject* seq = PySequence_Fast(invs, "inventories must be a sequence");
@@ -198,8 +219,15 @@ PyObject* py_pack_rows(PyObject*, PyObject* args) {
   FracCache fc;
   const Py_ssize_t R = PySequence_Fast_GET_SIZE(seq);
   std::vector<int32_t> row_ptr(R + 1, 0);
-  std::vector<Seg> segs;
-  const i128 limit = (i128)1 << 53;
+  std::vector<RunSeg> segs;
+  bool wide = force_wide != 0 || K > kKRegular;
+  const i128 limit53 = (i128)1 << 53;
+  const i128 limit127 = (((i128)1 << 126) - 1) * 2 + 1;  // 2^127 - 1
+  auto range_error = [&](const char* what) {
+    Py_DECREF(seq);
+    PyErr_SetString(PyExc_ValueError, what);
+    return (PyObject*)nullptr;
+  };
   for (Py_ssize_t r = 0; r < R; ++r) {
     PyObject* inv = PySequence_Fast_GET_ITEM(seq, r);
     // model: (a, b, layer) -> multiplicity
@@ -226,15 +254,17 @@ PyObject* py_pack_rows(PyObject*, PyObject* args) {
       // runs of consecutive layers with equal (a, b, multiplicity)
       for (auto& kvp : model) {
         const int64_t a = std::get<0>(kvp.first), b = std::get<1>(kvp.first), layer = std::get<2>(kvp.first);
-        const int64_t unit = bpl * kvp.second;
+        const i128 u = (i128)bpl * kvp.second;
+        if (u > (i128)INT64_MAX) return range_error("segment bytes exceed 2^63: outside the exact range");
+        const int64_t unit = (int64_t)u;
         if (segs.size() > first) {
-          Seg& s = segs.back();
-          if (s.pipe == 0 && s.a == a && s.b == b && s.unit == unit && s.l1 == layer) {
-            s.l1 = (int32_t)(layer + 1);
+          RunSeg& sg = segs.back();
+          if (sg.pipe == 0 && sg.a == a && sg.b == b && sg.unit == unit && sg.l1 == layer) {
+            sg.l1 = (int32_t)(layer + 1);
             continue;
           }
         }
-        segs.push_back({(int32_t)layer, (int32_t)(layer + 1), (int32_t)a, (int32_t)b, 0, 0, unit});
+        segs.push_back({(int32_t)layer, (int32_t)(layer + 1), 0, a, b, unit});
       }
       if (!need.empty()) {
         std::map<std::tuple<int64_t, int64_t, int32_t, int64_t>, int64_t> cache;
@@ -248,13 +278,13 @@ PyObject* py_pack_rows(PyObject*, PyObject* args) {
             goto fail;
           }
           Py_ssize_t len;
-          const char* s = PyUnicode_AsUTF8AndSize(prid, &len);
-          if (!s) {
+          const char* str = PyUnicode_AsUTF8AndSize(prid, &len);
+          if (!str) {
             Py_DECREF(prid);
             Py_DECREF(cs);
             goto fail;
           }
-          auto it = need.find(std::string(s, len));
+          auto it = need.find(std::string(str, len));
           Py_DECREF(prid);
           if (it == need.end() || it->second.empty()) continue;
           PyObject *pl = PySequence_GetItem(t, 1), *plo = PySequence_GetItem(t, 2),
@@ -278,31 +308,50 @@ PyObject* py_pack_rows(PyObject*, PyObject* args) {
           const int64_t a = std::get<0>(kvp.first), b = std::get<1>(kvp.first), layer = std::get<3>(kvp.first);
           const int32_t d = std::get<2>(kvp.first);
           const int64_t tsum = kvp.second;
+          const i128 u = (i128)kv * tsum;
+          if (u > (i128)INT64_MAX) return range_error("segment bytes exceed 2^63: outside the exact range");
+          const int64_t unit = (int64_t)u;
           if (segs.size() > cfirst) {
-            Seg& s = segs.back();
-            if (s.pipe == d && s.a == a && s.b == b && s.unit == kv * tsum && s.l1 == layer && tsum != 0) {
-              s.l1 = (int32_t)(layer + 1);
+            RunSeg& sg = segs.back();
+            if (sg.pipe == d && sg.a == a && sg.b == b && sg.unit == unit && sg.l1 == layer && tsum != 0) {
+              sg.l1 = (int32_t)(layer + 1);
               continue;
             }
           }
           if (tsum == 0) continue;
-          segs.push_back({(int32_t)layer, (int32_t)(layer + 1), (int32_t)a, (int32_t)b, d, 0, kv * tsum});
+          segs.push_back({(int32_t)layer, (int32_t)(layer + 1), d, a, b, unit});
         }
       }
+      // every W numerator of this row is <= the sum of its segments' spans:
+      // < 2^53 keeps the regular (64-bit) encoding, else 128-bit numerators
       i128 bound = 0;
-      for (size_t i = first; i < segs.size(); ++i)
-        bound += (i128)(segs[i].l1 - segs[i].l0) * (segs[i].b - segs[i].a) * segs[i].unit;
-      if (bound >= limit) {
-        Py_DECREF(seq);
-        PyErr_SetString(PyExc_ValueError, "edge-weight numerator may exceed 2^53: outside the exact range");
-        return nullptr;
+      for (size_t i = first; i < segs.size(); ++i) {
+        const i128 span = (i128)(segs[i].l1 - segs[i].l0) * (segs[i].b - segs[i].a);
+        if (span != 0 && (i128)segs[i].unit > limit127 / span) return range_error("edge-weight numerator may exceed 2^127: outside the exact range");
+        const i128 term = span * segs[i].unit;
+        if (bound > limit127 - term) return range_error("edge-weight numerator may exceed 2^127: outside the exact range");
+        bound += term;
       }
+      if (bound >= limit53) wide = true;
     }
     row_ptr[r + 1] = (int32_t)segs.size();
   }
   Py_DECREF(seq);
-  return Py_BuildValue("(y#y#)", bptr(row_ptr), (Py_ssize_t)(row_ptr.size() * 4), bptr(segs),
-                       (Py_ssize_t)(segs.size() * sizeof(Seg)));
+  if (!wide) {
+    std::vector<Seg> out(segs.size());  // (scoped: the gotos above jump past it)
+    for (size_t i = 0; i < segs.size(); ++i)
+      out[i] = {segs[i].l0, segs[i].l1, (int32_t)segs[i].a, (int32_t)segs[i].b, segs[i].pipe, 0, segs[i].unit};
+    return Py_BuildValue("(y#y#O)", bptr(row_ptr), (Py_ssize_t)(row_ptr.size() * 4), bptr(out),
+                         (Py_ssize_t)(out.size() * sizeof(Seg)), Py_False);
+  }
+  {
+    std::vector<WideSeg> out(segs.size());
+    for (size_t i = 0; i < segs.size(); ++i)
+      out[i] = {segs[i].l0, segs[i].l1, segs[i].pipe, 0, segs[i].a, segs[i].b, segs[i].unit, {0, 0, 0}};
+    for (auto& x : row_ptr) x *= 2;  // two sk_segment slots per wide segment
+    return Py_BuildValue("(y#y#O)", bptr(row_ptr), (Py_ssize_t)(row_ptr.size() * 4), bptr(out),
+                         (Py_ssize_t)(out.size() * sizeof(WideSeg)), Py_True);
+  }
 fail:
   Py_DECREF(seq);
   return nullptr;

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "../../include/spotkm.h"
+#include "exact.cuh"
 
 namespace {
 
@@ -35,46 +36,8 @@ thread_local char g_perr[512] = "";
 
 typedef __int128 i128;
 
-// correctly rounded num / den (num >= 0, den > 0): the value float(Fraction) gives
-double rat_to_double(i128 num, int64_t den) {
-  if (num == 0) return 0.0;
-  const i128 lim = (i128)1 << 53;
-  if (num < lim && den < ((int64_t)1 << 53)) return (double)(int64_t)num / (double)den;
-  // scale so that the integer quotient has exactly 54 bits, then round half-even
-  auto bits = [](i128 x) {
-    int b = 0;
-    while (x > 0) {
-      x >>= 1;
-      ++b;
-    }
-    return b;
-  };
-  int s = 54 - (bits(num) - bits((i128)den));
-  i128 n = num, d = den;
-  if (s >= 0)
-    n <<= s;
-  else
-    d <<= -s;
-  i128 q = n / d, r = n % d;
-  while (q >= ((i128)1 << 54)) {  // adjust if the estimate was one bit long
-    r += (q & 1) * d;
-    q >>= 1;
-    d <<= 1;
-    --s;
-  }
-  while (q < ((i128)1 << 53)) {
-    n = r * 2;
-    q = q * 2 + n / d;
-    r = n % d;
-    ++s;
-  }
-  // q has 54 bits: keep 53, round half-even using the dropped bit and r
-  const bool half = q & 1;
-  q >>= 1;
-  const bool sticky = r != 0;
-  if (half && (sticky || (q & 1))) ++q;
-  return std::ldexp((double)(int64_t)q, -(s - 1));
-}
+// correctly rounded num / den: the value float(Fraction) gives (exact.cuh)
+using sk_exact::rat_to_double;
 
 struct Seg {
   int64_t lo, hi;

@@ -28,6 +28,7 @@
 #include <stdio.h>
 
 #include "../../include/spotkm.h"
+#include "exact.cuh"
 
 namespace {
 
@@ -87,6 +88,55 @@ __device__ __forceinline__ long long seg_num(const sk_segment& s, const Col& c) 
 // same value float(Fraction(N, K)) gives (domain.py:320).
 __device__ __forceinline__ double num_to_w(long long n, int K) {
   return __ddiv_rn(__ll2double_rn(n), (double)K);
+}
+
+// ---- general-range plans (SK_PLAN_GENERIC): 64-bit endpoints, 128-bit
+// numerators, one correctly rounded conversion (exact.cuh) -- the same
+// float(Fraction) value for inputs beyond the regular encoding's range
+
+typedef __int128 i128;
+
+struct ColW {
+  int d;
+  int s0, s1;
+  long long i0, i1;
+};
+
+__device__ __forceinline__ ColW col_of_w(const sk_plan& p, int c) {
+  const int m = c % p.M;
+  const int t = c / p.M;
+  const int st = t % p.P;
+  const int d = t / p.P;
+  const int q = p.L / p.P, r = p.L % p.P;
+  ColW o;
+  o.d = d + 1;
+  o.s0 = st * q + min(st, r);
+  o.s1 = o.s0 + q + (st < r ? 1 : 0);
+  const long long w = p.Kw / p.M;
+  o.i0 = (long long)m * w;
+  o.i1 = o.i0 + w;
+  return o;
+}
+
+__device__ __forceinline__ const sk_segment_wide& wide_at(const sk_segment* segs, int s) {
+  return *reinterpret_cast<const sk_segment_wide*>(segs + s);
+}
+
+__device__ __forceinline__ i128 seg_num_wide(const sk_segment_wide& s, const ColW& c) {
+  const int ol = min(s.l1, c.s1) - max(s.l0, c.s0);
+  const long long oi = (s.b < c.i1 ? s.b : c.i1) - (s.a > c.i0 ? s.a : c.i0);
+  if (ol <= 0 || oi <= 0) return 0;
+  if (s.pipe != 0 && s.pipe != c.d) return 0;
+  return (i128)ol * (i128)oi * (i128)s.unit;  // < 2^127: bounded on the host
+}
+
+__device__ __forceinline__ double weight_generic(const sk_plan& p, const int32_t* __restrict__ row_ptr,
+                                                 const sk_segment* __restrict__ segs, int r, int c) {
+  const ColW col = col_of_w(p, c);
+  const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
+  i128 acc = 0;
+  for (int s = s0; s < s1; s += 2) acc += seg_num_wide(wide_at(segs, s), col);
+  return sk_exact::rat_to_double(acc, p.Kw);
 }
 
 __device__ __forceinline__ double weight_at(const sk_plan& p, const int32_t* __restrict__ row_ptr,
@@ -227,6 +277,12 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
   const int C = p.D * p.P * p.M;
   const int c = 2 * (blockIdx.x * kW_TPB + threadIdx.x);
   if (c >= C) return;
+  if (p.flags & SK_PLAN_GENERIC) {  // block-uniform
+    double* o = W + p.f_off + (long long)r * C + c;
+    o[0] = weight_generic(p, row_ptr, segs, r, c);
+    if (c + 1 < C) o[1] = weight_generic(p, row_ptr, segs, r, c + 1);
+    return;
+  }
   const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
   const Col ca = col_of(p, c);
   const bool two = c + 1 < C;
@@ -391,7 +447,7 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
                                                  uint32_t zero_perm) {
   // LPG lanes per GPU group: small targets have few candidate slots per group
   const sk_plan p = plans[plan0 + blockIdx.y];
-  if (p.group != G) return;
+  if (p.group != G || (p.flags & SK_PLAN_GENERIC)) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
   const int lane = threadIdx.x & 31, sub = lane % LPG;
@@ -556,6 +612,150 @@ int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, 
 }
 
 // ---------------------------------------------------------------------------
+// K2a for general-range plans (SK_PLAN_GENERIC: fused groups up to 32,
+// 128-bit numerators, 64-bit K).  One warp per fused pair (a, b): the g x g
+// block is built in shared memory (lane l = block column l) and the
+// reference's _hungarian_max (mapping.py:71-122) runs with lane j - 1 owning
+// column j: per Dijkstra step every unused column updates its own slack and
+// predecessor, the warp argmin picks the lowest column among equal minima
+// (mapping.py:103-105), and the potential update touches distinct rows.
+// The fused weight goes to F; the matched weights and the permutation go to
+// the plan's side area (sk_fused_elems) for the outer KM's expansion.
+
+constexpr int kG_WARPS = 4;
+constexpr int kG_MAX = 32;
+
+__device__ __forceinline__ unsigned long long order_key_g(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  if ((b << 1) == 0ull) b = 0ull;  // -0.0 ties with +0.0, as under '<'
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(32 * kG_WARPS) k_fuse_generic(const sk_plan* __restrict__ plans, int plan0,
+                                                                const int32_t* __restrict__ row_ptr,
+                                                                const sk_segment* __restrict__ segs,
+                                                                double* __restrict__ F) {
+  __shared__ double s_w[kG_WARPS][kG_MAX][kG_MAX + 1];
+  __shared__ double s_u[kG_WARPS][kG_MAX + 1];
+  __shared__ int s_match[kG_WARPS][kG_MAX + 1];
+  __shared__ int s_way[kG_WARPS][kG_MAX + 1];
+  __shared__ int s_perm[kG_WARPS][kG_MAX];
+  const sk_plan p = plans[plan0 + blockIdx.y];
+  if (!(p.flags & SK_PLAN_GENERIC)) return;
+  const int g = p.group;
+  const int nA = p.rows / g, nB = (p.D * p.P * p.M) / g;
+  const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long pair = (long long)blockIdx.x * kG_WARPS + wi;
+  if (pair >= (long long)nA * nB) return;  // warp-uniform
+  const int a = (int)(pair / nB), b = (int)(pair % nB);
+  double(*w)[kG_MAX + 1] = s_w[wi];
+  double* u = s_u[wi];
+  int* match = s_match[wi];
+  int* way = s_way[wi];
+  const bool col_on = lane < g;  // column j = lane + 1
+  if (col_on) {
+    const ColW c = col_of_w(p, b * g + lane);
+    for (int k = 0; k < g; ++k) {
+      const int r = a * g + k;
+      i128 acc = 0;
+      for (int s = row_ptr[p.row_base + r]; s < row_ptr[p.row_base + r + 1]; s += 2)
+        acc += seg_num_wide(wide_at(segs, s), c);
+      w[k][lane] = sk_exact::rat_to_double(acc, p.Kw);
+    }
+  }
+  if (lane <= g) {
+    u[lane] = 0.0;
+    match[lane] = 0;
+  }
+  __syncwarp();
+  double v = 0.0, minv = kInf;
+  int wr = 0;
+  for (int i = 1; i <= g; ++i) {
+    if (lane == 0) match[0] = i;
+    __syncwarp();
+    bool used = false;
+    minv = kInf;
+    int j0 = 0;
+    while (true) {
+      const int i0 = match[j0];
+      const double ui0 = u[i0];
+      const bool on = col_on && !used;
+      if (on) {
+        const double cur = (-w[i0 - 1][lane] - ui0) - v;
+        if (cur < minv) {
+          minv = cur;
+          wr = j0;
+        }
+      }
+      const unsigned long long key = on ? order_key_g(minv) : ~0ull;
+      const unsigned hi = __reduce_min_sync(kFull, (unsigned)(key >> 32));
+      const bool c1 = (unsigned)(key >> 32) == hi;
+      const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
+      const bool c2 = c1 && (unsigned)key == lo;
+      const unsigned jw = __reduce_min_sync(kFull, c2 && on ? (unsigned)(lane + 1) : 0xffffffffu);
+      const double delta = __shfl_sync(kFull, minv, (int)(jw - 1) & 31);
+      // u[match[j]] += delta, v[j] -= delta for used j (incl. column 0);
+      // minv[j] -= delta otherwise
+      if (lane == 0) u[match[0]] += delta;
+      if (col_on && used) {
+        u[match[lane + 1]] += delta;
+        v -= delta;
+      } else if (col_on) {
+        minv -= delta;
+      }
+      __syncwarp();
+      j0 = (int)jw;
+      if (lane + 1 == j0) used = true;
+      if (match[j0] == 0) break;
+    }
+    if (col_on) way[lane + 1] = wr;
+    __syncwarp();
+    if (lane == 0) {
+      while (j0) {
+        const int j1 = way[j0];
+        match[j0] = match[j1];
+        j0 = j1;
+      }
+    }
+    __syncwarp();
+  }
+  if (col_on) s_perm[wi][match[lane + 1] - 1] = lane;
+  __syncwarp();
+  const long long nAB = (long long)nA * nB;
+  double* side_w = F + p.f_off + nAB;
+  unsigned char* side_p = reinterpret_cast<unsigned char*>(F + p.f_off + nAB * (1 + g));
+  if (col_on) {
+    side_w[pair * g + lane] = w[lane][s_perm[wi][lane]];
+    side_p[pair * g + lane] = (unsigned char)s_perm[wi][lane];
+  }
+  if (lane == 0) {
+    double f;
+    if (p.flags & SK_PLAN_FUSED_SUM) {
+      // CPython >= 3.12 builtin sum (see py_builtin_sum)
+      f = 0.0 + w[0][s_perm[wi][0]];
+      double c = 0.0;
+      for (int k = 1; k < g; ++k) {
+        const double xi = w[k][s_perm[wi][k]];
+        const double t = f + xi;
+        if (fabs(f) >= fabs(xi))
+          c += (f - t) + xi;
+        else
+          c += (xi - t) + f;
+        f = t;
+      }
+      if (c != 0.0 && isfinite(c)) f += c;
+    } else {
+      f = w[0][s_perm[wi][0]];
+      for (int k = 1; k < g; ++k) {
+        const double x = w[k][s_perm[wi][k]];
+        if (x > f) f = x;
+      }
+    }
+    F[p.f_off + pair] = f;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2b: outer KM, one warp per plan.
 //
 // Column j (1..n) is owned by thread (j - 1) % T, slot k = (j - 1) / T (T =
@@ -663,6 +863,16 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
   unsigned long long b = (unsigned long long)__double_as_longlong(x);
   if ((b << 1) == 0ull) b = 0ull;  // -0.0 ties with +0.0, as under '<'
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// expansion of a general-range plan's matched pair: member k's column offset
+// and matched weight from the side area (kept out of line: the regular
+// plans' register allocation must not pay for it)
+__device__ __noinline__ double generic_pick(const double* Fp, long long nAB, int g, long long pair, int k,
+                                            int* col) {
+  const long long e = pair * g + k;
+  *col += reinterpret_cast<const unsigned char*>(Fp + nAB * (1 + g))[e];
+  return Fp[nAB + e];
 }
 
 // W = warps per plan.  W == 1: one warp per plan, several plans per block,
@@ -973,9 +1183,18 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
     const int b = way[a];
     if (b < nB) {
       int col = b * g;
-      if (g > 1)
-        col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
-      const double w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
+      double w;
+      if (p.flags & SK_PLAN_GENERIC) {
+        // matched weights and permutation from the plan's side area
+        const long long nAB = (long long)nA * nB;
+        const long long e = ((long long)a * nB + b) * g + k;
+        col += reinterpret_cast<const unsigned char*>(Fp + nAB * (1 + g))[e];
+        w = Fp[nAB + e];
+      } else {
+        if (g > 1)
+          col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
+        w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
+      }
       out[r] = col;
       wv[r] = w;
     } else {
@@ -1013,6 +1232,188 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
     }
     A.total[q] = t;
   }
+}
+
+// ---------------------------------------------------------------------------
+// K2b for outer problems beyond the register-resident shapes (n > 4095):
+// one 1024-thread CTA per plan runs the reference's _hungarian_max
+// (mapping.py:71-122) literally, with the per-column state (u, v, minv,
+// match, way, used) in a per-plan device scratch.  Thread t scans columns
+// t + 1, t + 1 + 1024, ... (ascending, first minimum), the block argmin keeps
+// the lowest column among equal minima, and the potential update touches
+// distinct rows -- the same results as the sequential scan at any n.
+
+constexpr int kH_TPB = 1024;
+
+__host__ __device__ __forceinline__ size_t huge_stride(int max_n, int max_rows) {
+  const size_t n1 = (size_t)max_n + 1;
+  return ((n1 * (3 * 8 + 2 * 4 + 1) + 8 + (size_t)max_rows * 8) + 255) & ~(size_t)255;
+}
+
+__global__ void __launch_bounds__(kH_TPB) k_outer_huge(const OuterArgs A, unsigned char* __restrict__ scratch,
+                                                       size_t stride) {
+  __shared__ unsigned long long s_key[kH_TPB / 32];
+  __shared__ unsigned s_j[kH_TPB / 32];
+  __shared__ double s_val[kH_TPB / 32];
+  __shared__ int s_j1;
+  __shared__ double s_delta;
+  const int q = blockIdx.x;
+  if (q >= A.n_plans) return;
+  const sk_plan p = A.plans[q];
+  const int g = p.group;
+  const bool dense = (p.flags & SK_PLAN_DENSE) != 0;
+  const int C = p.D * p.P * p.M;
+  const int nA = p.rows / g, nB = C / g;
+  const int n = nA > nB ? nA : nB;
+  const int t = threadIdx.x, lane = t & 31, wi = t >> 5;
+  const size_t n1 = (size_t)n + 1;
+  unsigned char* base = scratch + (size_t)q * stride;
+  double* u = reinterpret_cast<double*>(base);
+  double* v = u + n1;
+  double* minv = v + n1;
+  int* match = reinterpret_cast<int*>(minv + n1);
+  int* way = match + n1;
+  unsigned char* used = reinterpret_cast<unsigned char*>(way + n1);
+  double* wv = reinterpret_cast<double*>(base + ((n1 * (3 * 8 + 2 * 4 + 1) + 7) & ~(size_t)7));
+  const double* Fp = A.F + p.f_off;
+  for (int j = t; j <= n; j += kH_TPB) {
+    u[j] = 0.0;
+    v[j] = 0.0;
+    match[j] = 0;
+    way[j] = 0;
+  }
+  __syncthreads();
+  for (int i = 1; i <= n; ++i) {
+    for (int j = t; j <= n; j += kH_TPB) {
+      minv[j] = kInf;
+      used[j] = 0;
+    }
+    if (t == 0) match[0] = i;
+    __syncthreads();
+    int j0 = 0;
+    while (true) {
+      if (t == 0) used[j0] = 1;
+      __syncthreads();
+      const int i0 = match[j0];
+      const double ui0 = u[i0];
+      const double* row = Fp + (long long)(i0 - 1) * nB;
+      double best = kInf;
+      unsigned bj = 0xffffffffu;
+      for (int j = t + 1; j <= n; j += kH_TPB) {
+        if (used[j]) continue;
+        const double wgt = (i0 - 1 < nA && j - 1 < nB) ? row[j - 1] : 0.0;
+        const double cur = (-wgt - ui0) - v[j];
+        double mv = minv[j];
+        if (cur < mv) {
+          mv = cur;
+          minv[j] = cur;
+          way[j] = j0;
+        }
+        if (mv < best) {
+          best = mv;
+          bj = (unsigned)j;
+        }
+      }
+      // block argmin on (value, lowest j)
+      const unsigned long long key = bj == 0xffffffffu ? ~0ull : order_key_g(best);
+      const unsigned hi = __reduce_min_sync(kFull, (unsigned)(key >> 32));
+      const bool c1 = (unsigned)(key >> 32) == hi;
+      const unsigned lo = __reduce_min_sync(kFull, c1 ? (unsigned)key : 0xffffffffu);
+      const bool c2 = c1 && (unsigned)key == lo;
+      const unsigned jw = __reduce_min_sync(kFull, c2 ? bj : 0xffffffffu);
+      const unsigned src = __ffs(__ballot_sync(kFull, c2 && bj == jw)) - 1;
+      const double dv = __shfl_sync(kFull, best, src);
+      if (lane == 0) {
+        s_key[wi] = ((unsigned long long)hi << 32) | lo;
+        s_j[wi] = jw;
+        s_val[wi] = dv;
+      }
+      __syncthreads();
+      if (t == 0) {
+        unsigned long long bk = s_key[0];
+        unsigned bjj = s_j[0];
+        double bv = s_val[0];
+        for (int w = 1; w < kH_TPB / 32; ++w)
+          if (s_key[w] < bk || (s_key[w] == bk && s_j[w] < bjj)) {
+            bk = s_key[w];
+            bjj = s_j[w];
+            bv = s_val[w];
+          }
+        s_j1 = (int)bjj;
+        s_delta = bv;
+      }
+      __syncthreads();
+      const double delta = s_delta;
+      const int j1 = s_j1;
+      for (int j = t; j <= n; j += kH_TPB) {
+        if (used[j]) {
+          u[match[j]] += delta;
+          v[j] -= delta;
+        } else {
+          minv[j] -= delta;
+        }
+      }
+      __syncthreads();
+      j0 = j1;
+      if (match[j0] == 0) break;
+    }
+    if (t == 0) {
+      while (j0) {
+        const int j1 = way[j0];
+        match[j0] = match[j1];
+        j0 = j1;
+      }
+    }
+    __syncthreads();
+  }
+  // row_to_col for real fused rows -> way[] (free now), then the expansion
+  for (int j = t + 1; j <= n; j += kH_TPB) {
+    const int r = match[j];
+    if (r >= 1 && r <= nA) way[r - 1] = j - 1;
+  }
+  __syncthreads();
+  const bool generic = (p.flags & SK_PLAN_GENERIC) != 0;
+  const long long nAB = (long long)nA * nB;
+  int32_t* out = A.assign + p.out_off;
+  for (int r = t; r < p.rows; r += kH_TPB) {
+    const int a = r / g, k = r % g;
+    const int b = way[a];
+    if (b < nB) {
+      int col = b * g;
+      double w;
+      if (generic) {
+        w = generic_pick(Fp, nAB, g, (long long)a * nB + b, k, &col);
+      } else {
+        if (g > 1)
+          col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
+        w = dense ? Fp[(long long)r * nB + col] : weight_at(p, A.row_ptr, A.segs, r, col);
+      }
+      out[r] = col;
+      wv[r] = w;
+    } else {
+      out[r] = -1;
+      wv[r] = -1.0;
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+    for (int r = 0; r < p.rows; ++r)
+      if (wv[r] >= 0.0) tot += wv[r];
+    A.total[q] = tot;
+    if (A.steps) A.steps[2 * q] = A.steps[2 * q + 1] = 0;
+  }
+}
+
+int launch_outer_huge(const OuterArgs& A, int max_rows, cudaStream_t s) {
+  const size_t stride = huge_stride(A.max_n, max_rows);
+  void* scratch = nullptr;
+  if (cudaMallocAsync(&scratch, stride * (size_t)A.n_plans, s) != cudaSuccess)
+    return cuda_check("outer KM scratch (cudaMallocAsync)");
+  k_outer_huge<<<A.n_plans, kH_TPB, 0, s>>>(A, static_cast<unsigned char*>(scratch), stride);
+  int rc = cuda_check("k_outer_huge launch");
+  cudaFreeAsync(scratch, s);
+  return rc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1230,7 +1631,7 @@ int launch_outer(OuterArgs A, int max_rows, size_t codes_bytes, cudaStream_t s) 
 // one 2-, 4- or 8-warp block per plan.
 int outer_dispatch(const OuterArgs& A, int max_rows, size_t codes_bytes, cudaStream_t s) {
   int cpl = 0, w = 0;
-  if (A.max_n > 4095) return set_err(SK_EINVAL, "outer KM size %d exceeds 4095", A.max_n);
+  if (A.max_n > 4095) return launch_outer_huge(A, max_rows, s);
   outer_shape(A.max_n, &cpl, &w);
 #define SK_OUTER_CASE(C, WW) \
   if (cpl == C && w == WW) return launch_outer<C, WW>(A, max_rows, codes_bytes, s);
@@ -1254,6 +1655,12 @@ constexpr int kMaxGridY = 65535;
 extern "C" {
 
 int sk_abi_version(void) { return SPOTKM_ABI_VERSION; }
+
+int64_t sk_fused_elems(int32_t nA, int32_t nB, int32_t group, int32_t flags) {
+  const int64_t pairs = (int64_t)nA * nB;
+  if (!(flags & SK_PLAN_GENERIC)) return pairs;
+  return pairs * (1 + group) + (pairs * group + 7) / 8;
+}
 
 const char* sk_last_error(void) { return g_err; }
 
@@ -1287,10 +1694,17 @@ int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
   if (((long long)max_na * max_nb + kF_TPB - 1) / kF_TPB > 0x7fffffffLL)
     return set_err(SK_EINVAL, "too many fused pairs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int mask = group_mask ? group_mask : 0x1fe;
+  const int mask = group_mask ? group_mask : 0x1ff;
   for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
     const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
     int rc = SK_OK;
+    if (mask & 1) {  // general-range plans: one warp per fused pair
+      const long long pairs = (long long)max_na * max_nb;
+      if ((pairs + kG_WARPS - 1) / kG_WARPS > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
+      dim3 grid((unsigned)((pairs + kG_WARPS - 1) / kG_WARPS), np);
+      k_fuse_generic<<<grid, 32 * kG_WARPS, 0, s>>>(d_plans, p0, d_row_ptr, d_segs, d_fused);
+      rc = cuda_check("k_fuse_generic launch");
+    }
     if (!rc && (mask & (1 << 1))) rc = launch_fuse<1>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
     if (!rc && (mask & (1 << 2))) rc = launch_fuse<2>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);
     if (!rc && (mask & (1 << 3))) rc = launch_fuse<3>(d_plans, p0, np, max_na, max_nb, d_row_ptr, d_segs, d_fused, d_perm, s);

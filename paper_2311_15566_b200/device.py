@@ -19,6 +19,14 @@ def _align(n: int, a: int = 64) -> int:
     return (n + a - 1) // a * a
 
 
+def fused_elems(nA: int, nB: int, g: int, flags: int) -> int:
+    """Fused-buffer elements of one plan (include/spotkm.h sk_fused_elems)."""
+    pairs = nA * nB
+    if not flags & nat.SK_PLAN_GENERIC:
+        return pairs
+    return pairs * (1 + g) + (pairs * g + 7) // 8
+
+
 def _device():
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2311_15566_b200 needs a CUDA device (no CPU fallback)")
@@ -59,8 +67,11 @@ class MapBatch:
             R, D, P, M, L, K, g, flags = self.plans[q]
             C = D * P * M
             nA, nB = R // g, C // g
-            pairs = R * C if dense_cols else nA * nB
-            plans[slot] = (R, D, P, M, L, K, g, flags, row_base, 0, f_off, out_off, 0)
+            pairs = R * C if dense_cols else fused_elems(nA, nB, g, flags)
+            generic = bool(flags & nat.SK_PLAN_GENERIC)
+            # general-range plans carry K in Kw (sk_plan.K = 0)
+            plans[slot] = (R, D, P, M, L, 0 if generic else K, g, flags, row_base, 0, f_off, out_off,
+                           K if generic else 0)
             rp_parts.append(self.row_ptrs[q][:-1].astype(np.int64) + seg_base)
             seg_parts.append(self.segs[q])
             seg_base += len(self.segs[q])
@@ -73,7 +84,7 @@ class MapBatch:
             max_nb = max(max_nb, nB)
             max_rows = max(max_rows, R)
             max_cols = max(max_cols, C)
-            gmask |= 1 << g
+            gmask |= 1 if generic else 1 << g
         rp_parts.append(np.array([seg_base], dtype=np.int64))
         row_ptr = np.concatenate(rp_parts).astype(np.int32)
         segs = np.concatenate(seg_parts) if seg_parts else np.zeros(0, dtype=nat.SEGMENT)

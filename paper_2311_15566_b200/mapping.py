@@ -89,10 +89,11 @@ def required_context_with_cache(config, pos, model, inherited, inventory_cls=Non
 # problem packing
 
 class _Problem:
-    __slots__ = ("refs", "rows", "D", "P", "M", "L", "K", "row_ptr", "segs")
+    __slots__ = ("refs", "rows", "D", "P", "M", "L", "K", "row_ptr", "segs", "wide")
 
 
-def _pack_problem(instances, target, model, inheritance, requests_by_old_pipeline, err):
+def _pack_problem(instances, target, model, inheritance, requests_by_old_pipeline, err,
+                  force_wide=False):
     prob = _Problem()
     refs, invs = [], []
     for inst in sorted(instances, key=lambda i: natural_key(i.id)):
@@ -106,8 +107,9 @@ def _pack_problem(instances, target, model, inheritance, requests_by_old_pipelin
     need = need_tokens(inherited_by_new(inheritance, requests_by_old_pipeline), prob.D)
     try:
         prob.K = common_denominator(invs, prob.M)
-        prob.row_ptr, prob.segs = pack_rows(invs, prob.K, model.bytes_per_layer,
-                                            model.kv_bytes_per_token_per_layer, need)
+        prob.row_ptr, prob.segs, prob.wide = pack_rows(invs, prob.K, model.bytes_per_layer,
+                                                       model.kv_bytes_per_token_per_layer, need,
+                                                       force_wide)
     except PackError as e:
         raise err(str(e)) from None
     return prob
@@ -132,7 +134,8 @@ def build_graph(instances, target, model, inheritance=None, requests_by_old_pipe
     if prob.rows == 0:
         return T.BipartiteGraph(gpus=[], slots=slots, weights=[])
     batch = MapBatch()
-    batch.add(prob.rows, prob.D, prob.P, prob.M, prob.L, prob.K, 1, 0, prob.row_ptr, prob.segs)
+    batch.add(prob.rows, prob.D, prob.P, prob.M, prob.L, prob.K, 1,
+              nat.SK_PLAN_GENERIC if prob.wide else 0, prob.row_ptr, prob.segs)
     (W,) = batch.run_weights(T.MappingError)
     return T.BipartiteGraph(gpus=prob.refs, slots=slots, weights=W.tolist())
 
@@ -167,8 +170,9 @@ def _validate(instances, target, gpus_per_instance, fused_weight, T):
             raise T.MappingError(
                 f"group size {group} must divide both G={gpus_per_instance} "
                 f"and M={target.tensor_shards}")
-    if group > 8:
-        raise T.MappingError(f"fused group {group} > 8 is not supported by the device matcher")
+    if group > nat.MAX_GENERIC_GROUP:
+        raise T.MappingError(f"fused group {group} > {nat.MAX_GENERIC_GROUP} GPUs is not supported "
+                             "by the device matcher")
     return group
 
 
@@ -194,8 +198,13 @@ def map_devices_many(problems):
         fused_weight = args[6] if len(args) > 6 else "max"
         T = result_types(target)
         group = _validate(instances, target, G, fused_weight, T)
-        prob = _pack_problem(instances, target, model, inheritance, reqs, T.MappingError)
+        # fused groups > 8 take the general-range kernels (so do numerators
+        # >= 2^53 and denominators > 2^31 - 1, detected by the packer)
+        prob = _pack_problem(instances, target, model, inheritance, reqs, T.MappingError,
+                             force_wide=group > 8)
         flags = nat.SK_PLAN_FUSED_SUM if fused_weight == "sum" else 0
+        if prob.wide:
+            flags |= nat.SK_PLAN_GENERIC
         idx = None
         if prob.rows:
             idx = batch.add(prob.rows, prob.D, prob.P, prob.M, prob.L, prob.K, group, flags,

@@ -22,10 +22,12 @@ from math import lcm
 
 import numpy as np
 
-from ._native import SEGMENT
+from ._native import SEGMENT, SEGMENT_WIDE
 
-EXACT_LIMIT = 1 << 53
-K_LIMIT = (1 << 31) - 1
+EXACT_LIMIT = 1 << 53       # regular encoding: numerators exact in int64 -> double
+K_LIMIT = (1 << 31) - 1     # regular encoding: int32 endpoints
+WIDE_LIMIT = 1 << 127       # general-range encoding: 128-bit numerators
+K_WIDE_LIMIT = 1 << 62      # general-range encoding: 64-bit endpoints
 
 
 class PackError(ValueError):
@@ -62,8 +64,8 @@ def py_common_denominator(inventories, tensor_shards: int) -> int:
     K = 1
     for d in dens:
         K = lcm(K, d)
-    if K > K_LIMIT:
-        raise PackError(f"common interval denominator {K} exceeds 2^31-1")
+        if K >= K_WIDE_LIMIT:
+            raise PackError("common interval denominator exceeds 2^62")
     return K
 
 
@@ -142,32 +144,45 @@ def pack_row(inv, K: int, bpl: int, kv: int, need: dict):
     return segs
 
 
-def pack_rows(inventories, K: int, bpl: int, kv: int, need: dict):
-    """-> (row_ptr int32[R+1], segments SEGMENT[S]) via the native packer
-    (csrc/hostpack.cpp), identical to py_pack_rows."""
+def pack_rows(inventories, K: int, bpl: int, kv: int, need: dict, wide: bool = False):
+    """-> (row_ptr int32[R+1], segments, wide) via the native packer
+    (csrc/hostpack.cpp), identical to py_pack_rows.  `wide` (returned): the
+    rows are encoded as sk_segment_wide (two SEGMENT slots each) for the
+    general-range kernels -- forced by the caller, or because K > 2^31 - 1 or
+    a numerator may reach 2^53."""
     try:
-        rp, sg = _native().pack_rows(inventories, K, bpl, kv, need)
+        rp, sg, w = _native().pack_rows(inventories, K, bpl, kv, need, bool(wide))
     except ValueError as e:
         raise PackError(str(e)) from None
-    return np.frombuffer(rp, dtype=np.int32).copy(), np.frombuffer(sg, dtype=SEGMENT).copy()
+    segs = np.frombuffer(sg, dtype=SEGMENT_WIDE if w else SEGMENT).copy()
+    if w:
+        segs = segs.view(SEGMENT)
+    return np.frombuffer(rp, dtype=np.int32).copy(), segs, bool(w)
 
 
-def py_pack_rows(inventories, K: int, bpl: int, kv: int, need: dict):
+def py_pack_rows(inventories, K: int, bpl: int, kv: int, need: dict, wide: bool = False):
     """Pure-Python statement of pack_rows: the readable spec the native packer
     is tested against (tests/test_pack.py)."""
     rows = [pack_row(inv, K, bpl, kv, need) for inv in inventories]
+    wide = wide or K > K_LIMIT
     row_ptr = np.zeros(len(rows) + 1, dtype=np.int32)
     total = 0
     for i, segs in enumerate(rows):
+        if any(s[5] >= 1 << 63 for s in segs):
+            raise PackError("segment bytes exceed 2^63: outside the exact range")
         # every W numerator of this row is <= the sum of its segments' spans
-        if sum((s[1] - s[0]) * (s[3] - s[2]) * s[5] for s in segs) >= EXACT_LIMIT:
-            raise PackError("edge-weight numerator may exceed 2^53: outside the exact range")
+        bound = sum((s[1] - s[0]) * (s[3] - s[2]) * s[5] for s in segs)
+        if bound >= WIDE_LIMIT:
+            raise PackError("edge-weight numerator may exceed 2^127: outside the exact range")
+        wide = wide or bound >= EXACT_LIMIT
         total += len(segs)
         row_ptr[i + 1] = total
-    out = np.zeros(total, dtype=SEGMENT)
+    dt = SEGMENT_WIDE if wide else SEGMENT
+    out = np.zeros(total, dtype=dt)
     if total:
-        arr = np.array([s for segs in rows for s in segs], dtype=np.int64)
-        for f, col in (("l0", 0), ("l1", 1), ("a", 2), ("b", 3), ("pipe", 4)):
-            out[f] = arr[:, col]
-        out["unit"] = arr[:, 5]
-    return row_ptr, out
+        arr = np.array([s for segs in rows for s in segs], dtype=object)
+        for f, col in (("l0", 0), ("l1", 1), ("a", 2), ("b", 3), ("pipe", 4), ("unit", 5)):
+            out[f] = arr[:, col].astype(np.int64)
+    if wide:
+        return row_ptr * 2, out.view(SEGMENT), True
+    return row_ptr, out, False

@@ -141,6 +141,8 @@ def _align(n: int, a: int = 256) -> int:
 def cpl_bucket(n: int):
     """(warps per plan, columns per thread) of the outer-KM template the
     dispatch picks for size n (mirrors outer_dispatch in spotkm.cu)."""
+    if n > 4095:
+        return (32, 0)   # k_outer_huge: one 1024-thread CTA per plan
     need = max(1, (n + 31) // 32)
     if need <= 6:
         return (1, need)

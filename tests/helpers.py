@@ -35,3 +35,18 @@ def assignment_cols(mapping, instances, cfg):
             pos = mapping.assignment.get((inst.id, g))
             out.append(-1 if pos is None else col[pos])
     return out
+
+
+def own_from_port(instances, new, G, inh, reqs, model_geom):
+    """oracle-port plain values (oracle.sweep_inputs.plan_to_port) -> this
+    package's own domain objects, for the drop-in map_devices."""
+    L, bpl, kv = model_geom
+    mspec = sk.ModelSpec(name="m", num_layers=L, bytes_per_layer=bpl, kv_bytes_per_token_per_layer=kv)
+    insts = [sk.InstanceState(id=iid, kind="spot", gpus=G,
+                              gpu_inventories=[sk.ContextInventory(model_shards=tuple(i.model),
+                                                                   cache_shards=tuple(i.cache))
+                                               for i in invs])
+             for iid, invs in instances]
+    rq = {d: [sk.RequestSpec(id=rid, arrival_time=0.0, s_in=tok, s_out=max(tok, 1)) for rid, tok in lst]
+          for d, lst in reqs.items()}
+    return mspec, sk.ParallelConfig(*new, 1), insts, rq

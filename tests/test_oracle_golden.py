@@ -26,10 +26,10 @@ def test_km_cases_bit_exact(golden):
         assert n >= 1
 
 
-@pytest.mark.parametrize("name", ["mapping", "scenario"])
+@pytest.mark.parametrize("name", ["mapping", "scenario", "edge", "models_bs"])
 def test_mapping_cases_bit_exact(golden, name):
     doc = golden(name)
-    cases = doc["cases"] if name == "mapping" else doc["maps"]
+    cases = doc["maps"] if name in ("scenario", "models_bs") else doc["cases"]
     n_checked = 0
     for case in cases:
         model, target, G, instances, inh, reqs, fw = decode_map_case(case)
@@ -69,3 +69,41 @@ def test_permutation_pattern_blocks_match_their_permutation():
                 W[k][sig[k]] = float(rng.choice([rng.random() * 1e9, 1.0, 5e-324, 1e300,
                                                  rng.integers(1, 10) / 3]))
             assert port.hungarian_max(W) == list(sig)
+
+
+def test_km_wide_cases_bit_exact(golden):
+    """huge / subnormal weights (round-2 goldens, gen_golden_r2.py)"""
+    for case in golden("edge")["km"]:
+        W = [[unhx(x) for x in row] for row in case["W"]]
+        assign, total = port.km_flat(W, len(W), len(W[0]))
+        assert assign == case["assign"]
+        assert total.hex() == case["total"]
+
+
+def test_sweep_plans_bit_exact_vs_reference(golden):
+    """Plans of the headline sweep (64..1024 positions) solved by the real
+    reference: the oracle port and the C oracle agree with it."""
+    import numpy as np
+
+    from cases import plan_digest
+    from oracle import cport
+    from oracle.sweep_inputs import plan_to_port
+    from paper_2311_15566_b200 import sweep
+
+    cases = golden("sweep_ref")["cases"]
+    assert {c["N"] for c in cases} == {64, 128, 256, 512, 1024}
+    batches = {}
+    for c in cases:
+        b = batches.get(c["N"])
+        if b is None:
+            b = batches[c["N"]] = sweep.make_sweep(c["N"], c["sets"], seed=c["seed"])
+        q = c["q"]
+        assert plan_digest(b, q) == c["digest"]
+        exp_assign, exp_tot = cport.map_sweep(b.desc[q:q + 1], b.plans, b.alive, b.tok)
+        o, R = int(b.plans["out_off"][q]), int(b.plans["rows"][q])
+        assert exp_assign[o:o + R].tolist() == c["assign"] and exp_tot[q].hex() == c["total"]
+        if c["N"] <= 128:   # the Python port is slow at the big sizes
+            inst, new, G, inh, reqs, fw = plan_to_port(b, q, sweep.GPT20B, n_requests=4)
+            _, _, _, assign, total = port.map_devices(inst, new, sweep.GPT20B, G, inh, reqs, fw)
+            assert assign == c["assign"] and total.hex() == c["total"]
+    _ = np

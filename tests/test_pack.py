@@ -12,7 +12,7 @@ from paper_2311_15566_b200 import pack
 from paper_2311_15566_b200.domain import natural_key
 
 
-def eval_w(row_ptr, segs, K, cfg, L):
+def eval_w(row_ptr, segs, K, cfg, L, wide=False):
     D, P, M = cfg.data_parallel, cfg.pipeline_stages, cfg.tensor_shards
     cols = []
     for d in range(D):
@@ -23,6 +23,9 @@ def eval_w(row_ptr, segs, K, cfg, L):
                 s1 = s0 + q + (1 if p < r else 0)
                 w = K // M
                 cols.append((d + 1, s0, s1, m * w, m * w + w))
+    if wide:  # two SEGMENT slots per sk_segment_wide; row_ptr counts slots
+        segs = segs.view(pack.SEGMENT_WIDE)
+        row_ptr = row_ptr // 2
     W = []
     for i in range(len(row_ptr) - 1):
         row = []
@@ -39,11 +42,11 @@ def eval_w(row_ptr, segs, K, cfg, L):
     return W
 
 
-@pytest.mark.parametrize("name", ["mapping", "scenario"])
+@pytest.mark.parametrize("name", ["mapping", "scenario", "edge"])
 def test_segments_reproduce_golden_weights(golden, name):
     doc = golden(name)
-    cases = doc["cases"] if name == "mapping" else doc["maps"]
-    checked = 0
+    cases = doc["cases"] if name != "scenario" else doc["maps"]
+    checked = wide_seen = 0
     for case in cases:
         if "W" not in case:
             continue
@@ -51,18 +54,28 @@ def test_segments_reproduce_golden_weights(golden, name):
         invs = [inv for inst in sorted(insts, key=lambda i: natural_key(i.id))
                 for inv in inst.gpu_inventories]
         K = pack.common_denominator(invs, cfg.tensor_shards)
-        need = pack.need_tokens(pack.inherited_by_new(inh, rq))
-        row_ptr, segs = pack.pack_rows(invs, K, model.bytes_per_layer,
-                                       model.kv_bytes_per_token_per_layer, need)
-        W = eval_w(row_ptr, segs, K, cfg, model.num_layers)
+        need = pack.need_tokens(pack.inherited_by_new(inh, rq), cfg.data_parallel)
+        row_ptr, segs, wide = pack.pack_rows(invs, K, model.bytes_per_layer,
+                                             model.kv_bytes_per_token_per_layer, need)
+        W = eval_w(row_ptr, segs, K, cfg, model.num_layers, wide)
         assert [[x.hex() for x in row] for row in W] == case["W"]
         # the native packer (csrc/hostpack.cpp) equals the Python statement
         assert K == pack.py_common_denominator(invs, cfg.tensor_shards)
-        rp2, sg2 = pack.py_pack_rows(invs, K, model.bytes_per_layer,
-                                     model.kv_bytes_per_token_per_layer, need)
+        rp2, sg2, w2 = pack.py_pack_rows(invs, K, model.bytes_per_layer,
+                                         model.kv_bytes_per_token_per_layer, need)
+        assert w2 == wide
         assert rp2.tobytes() == row_ptr.tobytes() and sg2.tobytes() == segs.tobytes()
+        # forcing the general-range encoding keeps the weights
+        rp3, sg3, w3 = pack.pack_rows(invs, K, model.bytes_per_layer,
+                                      model.kv_bytes_per_token_per_layer, need, wide=True)
+        assert w3
+        W3 = eval_w(rp3, sg3, K, cfg, model.num_layers, True)
+        assert [[x.hex() for x in row] for row in W3] == case["W"]
         checked += 1
+        wide_seen += wide
     assert checked >= 10
+    if name == "edge":
+        assert wide_seen >= 10   # numerators >= 2^53 and K > 2^31 - 1 take the wide encoding
 
 
 def test_structured_row_is_one_model_and_one_cache_segment():
@@ -74,6 +87,7 @@ def test_structured_row_is_one_model_and_one_cache_segment():
     inv = ContextInventory(inv_m, inv_c)
     need = {f"r{j}": [(1, 600 + j)] for j in range(4)}
     segs = pack.pack_row(inv, 8, 1000, 16, need)
-    rp, sg = pack.pack_rows([inv], 8, 1000, 16, need)
+    rp, sg, wide = pack.pack_rows([inv], 8, 1000, 16, need)
+    assert not wide
     assert sg.tolist() == [(3, 9, 2, 4, 0, 0, 1000), (3, 9, 2, 4, 1, 0, 16 * (600 + 601 + 602 + 603))]
     assert segs == [(3, 9, 2, 4, 0, 1000), (3, 9, 2, 4, 1, 16 * (600 + 601 + 602 + 603))]
