@@ -46,3 +46,35 @@ def plan_to_port(batch, q, model, n_requests: int = 1):
     inh = {dd: dd for dd in range(1, min(oD, new[0]) + 1)}
     fw = "sum" if int(p["flags"]) & 1 else "max"
     return instances, new, G, inh, reqs, fw
+
+
+def plan_to_spotsim(batch, q, model_geom, spotsim, n_requests: int = 4):
+    """One sweep plan -> the REAL reference's objects (spotsim.domain), so the
+    reference's own map_devices can run on exactly the plan the GPU solves.
+    Returns the map_devices arguments (instances, target, model, G,
+    inheritance, requests_by_old_pipeline, fused_weight)."""
+    dm = spotsim.domain
+    instances, new, G, inh, reqs, fw = plan_to_port(batch, q, model_geom, n_requests=n_requests)
+    L, bpl, kv = model_geom
+    model = dm.ModelSpec(name="sweep", num_layers=L, bytes_per_layer=bpl, kv_bytes_per_token_per_layer=kv)
+    insts = []
+    for iid, invs in instances:
+        inst = dm.InstanceState(id=iid, kind="spot", gpus=G)
+        inst.gpu_inventories = [dm.ContextInventory(model_shards=tuple(i.model), cache_shards=tuple(i.cache))
+                                for i in invs]
+        insts.append(inst)
+    rq = {d: [dm.RequestSpec(id=rid, arrival_time=0.0, s_in=tok, s_out=max(tok, 1)) for rid, tok in lst]
+          for d, lst in reqs.items()}
+    return insts, dm.ParallelConfig(*new, 1), model, G, inh, rq, fw
+
+
+def mapping_cols(mapping, instances, target, spotsim):
+    """A DeviceMapping as assigned column per GPU row (reference row order)."""
+    slots = spotsim.domain.positions(target)
+    col = {s: j for j, s in enumerate(slots)}
+    out = []
+    for inst in sorted(instances, key=lambda i: spotsim.domain.natural_key(i.id)):
+        for g in range(inst.gpus):
+            pos = mapping.assignment.get((inst.id, g))
+            out.append(-1 if pos is None else col[pos])
+    return out
