@@ -224,6 +224,44 @@ typedef struct sk_copy {
 
 int sk_copy_batched(const sk_copy* d_copies, int n_copies, int n_ctas, void* stream);
 
+/*
+ * K3, plan-ordered: ONE persistent launch per rank executes the rank's share
+ * of a MigrationPlan round by round (migration.py:311-384).  CTA 0 monitors
+ * progress; workers copy 1 MiB chunks in plan order.  A chunk whose
+ * destination reuses arena space released at the end of round `wait_round`
+ * (the plan's `releases`, recycled by the host's arena allocator) waits until
+ * every rank has completed rounds 0..wait_round (their progress words,
+ * peer-mapped); no other cross-rank wait.  Stage-ready flags (start_stage,
+ * migration.py:352-371) are raised on the device as soon as global progress
+ * passes the round each marker follows, stamped with %globaltimer.
+ *   d_ctl: sk_exec_ctl_bytes(n_rounds, n_stages) bytes of device memory:
+ *     u32 [0] work_next [1] progress (rounds complete, read by peers)
+ *     [2] error (0 ok, 1 worker timeout, 2 monitor timeout) [3] reserved,
+ *     [4, 4+n_rounds) chunks done per round, then n_stages stage flags, then
+ *     (8-byte aligned) u64 stamps: launch start, each stage's ready time (ns).
+ *   d_peer_progress: device array of n_peers device pointers to the other
+ *     ranks' progress words (CUDA IPC mappings of their d_ctl + 1).
+ * The call resets d_ctl on `stream` first; ranks must not launch a new run
+ * before every peer has reset (a barrier between runs).
+ */
+typedef struct sk_exec_chunk {
+  uint64_t src, dst, bytes;
+  int32_t round;       /* plan round (non-start_stage action index) it belongs to */
+  int32_t wait_round;  /* -1, or: wait until every rank completed rounds 0..wait_round */
+} sk_exec_chunk; /* 32 bytes */
+
+int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages);
+int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_round_total, int n_rounds,
+                 const int32_t* d_stage_round, int n_stages, uint32_t* d_ctl,
+                 const uint32_t* const* d_peer_progress, int n_peers, int n_ctas, double timeout_s,
+                 void* stream);
+
+/* Copy-engine comparison path: one cudaMemcpyAsync per (HOST array) entry,
+ * in order, on `stream`.  sk_d2h: blocking device -> host copy (control
+ * block readback). */
+int sk_memcpy_batched(const sk_copy* h_copies, int n, void* stream);
+int sk_d2h(void* h_dst, const void* d_src, uint64_t bytes);
+
 /* Peer-access helper: enable access from `device` to each of `peers`. */
 int sk_enable_peer_access(int device, const int* peers, int n_peers);
 

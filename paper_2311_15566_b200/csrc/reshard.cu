@@ -65,6 +65,170 @@ __global__ void __launch_bounds__(kR_TPB) k_verify(const sk_region* __restrict__
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
 }
 
+// ---------------------------------------------------------------------------
+// k_exec: one persistent launch per rank executes the rank's share of a
+// MigrationPlan in plan order (migration.py:311-384; the paper's engine runs
+// it as batched async send/recv).
+//
+//   * CTA 0 is the monitor; CTAs 1.. are copy workers.
+//   * Workers take 1 MiB chunks in plan (round) order from an atomic work
+//     counter and copy them with 16-B vector loads/stores over the peer
+//     mapping (NVLink).  After a chunk every thread fences at system scope
+//     and the CTA bumps the round's done counter.
+//   * A chunk whose destination range reuses arena space freed at the end of
+//     round d (a plan `release`, recycled by the host-side arena allocator)
+//     first waits until EVERY rank has completed rounds 0..d -- so the old
+//     bytes are gone only when every reader of them is done.  This is the
+//     only cross-rank wait: rounds otherwise overlap, as the reference's
+//     timeline models them (costmodel.py:189-228).
+//   * The monitor publishes this rank's progress (rounds 0..p-1 complete) for
+//     the peers, and raises stage-ready flags (with a %globaltimer stamp) as
+//     soon as global progress passes the round each start_stage marker follows
+//     (migration.py:352-371) -- the device-side readiness signal a consumer
+//     (context daemon client) waits on with cuStreamWaitValue32 or a poll.
+//
+// Control block (u32 words, device memory, IPC-exportable):
+//   [0] work_next  [1] progress  [2] error  [3] reserved
+//   [4 .. 4+R)     done chunks per round
+//   then n_stages stage flags, then (8-B aligned) n_stages + 1 u64 stamps:
+//   the launch start and each stage's ready time (ns, %globaltimer).
+
+constexpr int kX_TPB = 512;
+
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+  return *reinterpret_cast<const volatile unsigned*>(p);
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct ExecArgs {
+  const sk_exec_chunk* chunks;
+  int n_chunks;
+  const unsigned* round_total;  // chunks per round issued by this rank
+  int n_rounds;
+  const int* stage_round;       // per stage: ready once rounds 0..stage_round complete (-1: at start)
+  int n_stages;
+  unsigned* ctl;
+  const unsigned* const* peer_progress;  // every OTHER rank's progress word
+  int n_peers;
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ unsigned* exec_flags(const ExecArgs& A) { return A.ctl + 4 + A.n_rounds; }
+__device__ __forceinline__ unsigned long long* exec_stamps(const ExecArgs& A) {
+  const size_t w = (size_t)4 + A.n_rounds + A.n_stages;
+  return reinterpret_cast<unsigned long long*>(A.ctl + ((w + 1) & ~(size_t)1));
+}
+
+__device__ unsigned global_progress(const ExecArgs& A) {
+  unsigned g = ld_volatile_u32(A.ctl + 1);
+  for (int i = 0; i < A.n_peers; ++i) {
+    const unsigned v = ld_volatile_u32(A.peer_progress[i]);
+    g = v < g ? v : g;
+  }
+  return g;
+}
+
+__global__ void __launch_bounds__(kX_TPB) k_exec(const ExecArgs A) {
+  __shared__ int s_idx;
+  __shared__ int s_abort;
+  const unsigned long long t0 = global_ns();
+  if (blockIdx.x == 0) {
+    // ---- monitor ----
+    if (threadIdx.x != 0) return;
+    unsigned* flags = exec_flags(A);
+    unsigned long long* stamps = exec_stamps(A);
+    stamps[0] = t0;
+    unsigned p = 0;
+    int pending = A.n_stages;
+    while (true) {
+      unsigned q = p;
+      while ((int)q < A.n_rounds && ld_volatile_u32(A.ctl + 4 + q) >= A.round_total[q]) ++q;
+      if (q != p) {
+        __threadfence_system();  // the rounds' data before the progress word
+        *reinterpret_cast<volatile unsigned*>(A.ctl + 1) = q;
+        p = q;
+      }
+      if (pending) {
+        const unsigned g = global_progress(A);
+        for (int s = 0; s < A.n_stages; ++s) {
+          if (flags[s] == 0u && (long long)A.stage_round[s] < (long long)g) {
+            stamps[1 + s] = global_ns();
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned*>(flags + s) = 1u;
+            --pending;
+          }
+        }
+      }
+      if ((int)p >= A.n_rounds && pending == 0) break;
+      if (ld_volatile_u32(A.ctl + 2) != 0u) break;
+      if (global_ns() - t0 > A.timeout_ns) {
+        atomicExch(A.ctl + 2, 2u);  // monitor timeout
+        break;
+      }
+      __nanosleep(200);
+    }
+    return;
+  }
+  // ---- workers ----
+  unsigned cached_g = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_idx = (int)atomicAdd(A.ctl + 0, 1u);
+      s_abort = 0;
+    }
+    __syncthreads();
+    const int idx = s_idx;
+    if (idx >= A.n_chunks) break;
+    const sk_exec_chunk c = A.chunks[idx];
+    if (c.wait_round >= 0 && cached_g <= (unsigned)c.wait_round) {
+      if (threadIdx.x == 0) {
+        // recycled space: every rank must be past round wait_round
+        while (true) {
+          cached_g = global_progress(A);
+          if (cached_g > (unsigned)c.wait_round) break;
+          if (ld_volatile_u32(A.ctl + 2) != 0u || global_ns() - t0 > A.timeout_ns) {
+            atomicCAS(A.ctl + 2, 0u, 1u);  // worker timeout
+            s_abort = 1;
+            break;
+          }
+          __nanosleep(500);
+        }
+        __threadfence_system();
+      }
+      __syncthreads();
+      if (s_abort) break;
+    }
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(c.src);
+    unsigned char* dst = reinterpret_cast<unsigned char*>(c.dst);
+    uint64_t done = 0;
+    if (((c.src | c.dst) & 15ull) == 0) {
+      const uint64_t nv = c.bytes >> 4;
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+      int4* d4 = reinterpret_cast<int4*>(dst);
+      uint64_t i = threadIdx.x;
+      constexpr int U = 8;
+      for (; i + (U - 1) * kX_TPB < nv; i += U * kX_TPB) {
+        int4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = __ldcs(s4 + i + u * kX_TPB);
+#pragma unroll
+        for (int u = 0; u < U; ++u) __stcs(d4 + i + u * kX_TPB, t[u]);
+      }
+      for (; i < nv; i += kX_TPB) __stcs(d4 + i, __ldcs(s4 + i));
+      done = nv << 4;
+    }
+    for (uint64_t i = done + threadIdx.x; i < c.bytes; i += kX_TPB) dst[i] = src[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(A.ctl + 4 + c.round, 1u);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -117,6 +281,53 @@ int sk_verify_regions(const sk_region* d_regions, int n, unsigned long long* d_b
 }
 
 const char* sk_reshard_error(void) { return g_rerr; }
+
+int sk_memcpy_batched(const sk_copy* h_copies, int n, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n; ++i) {
+    cudaError_t e = cudaMemcpyAsync(reinterpret_cast<void*>(h_copies[i].dst),
+                                    reinterpret_cast<const void*>(h_copies[i].src), h_copies[i].bytes,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return rfail("cudaMemcpyAsync", e);
+  }
+  return SK_OK;
+}
+
+int sk_d2h(void* h_dst, const void* d_src, uint64_t bytes) {
+  cudaError_t e = cudaMemcpy(h_dst, d_src, bytes, cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? SK_OK : rfail("cudaMemcpy D2H", e);
+}
+
+int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages) {
+  const int64_t w = 4 + (int64_t)n_rounds + n_stages;
+  return ((w + 1) & ~(int64_t)1) * 4 + 8 * (int64_t)(n_stages + 1);
+}
+
+int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_round_total, int n_rounds,
+                 const int32_t* d_stage_round, int n_stages, uint32_t* d_ctl,
+                 const uint32_t* const* d_peer_progress, int n_peers, int n_ctas, double timeout_s,
+                 void* stream) {
+  if (n_chunks < 0 || n_rounds < 0 || n_stages < 0 || n_peers < 0) {
+    snprintf(g_rerr, sizeof g_rerr, "negative sizes");
+    return SK_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // a fresh control block per run (the caller orders this before any peer
+  // reads it, e.g. with a barrier between sk_exec_plan calls of a new run)
+  cudaError_t e = cudaMemsetAsync(d_ctl, 0, (size_t)sk_exec_ctl_bytes(n_rounds, n_stages), s);
+  if (e != cudaSuccess) return rfail("exec control reset", e);
+  if (n_ctas <= 1) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    n_ctas = 2 * sms;  // two 512-thread CTAs per SM, all co-resident: the monitor + workers
+  }
+  ExecArgs A{d_chunks, n_chunks, d_round_total, n_rounds, d_stage_round, n_stages, d_ctl,
+             d_peer_progress, n_peers, (unsigned long long)(timeout_s * 1e9)};
+  k_exec<<<n_ctas, kX_TPB, 0, s>>>(A);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? SK_OK : rfail("k_exec launch", e);
+}
 
 }  // extern "C"
 

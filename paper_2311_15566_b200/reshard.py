@@ -1,20 +1,35 @@
 """Migration executor (K3): carry out a MigrationPlan's weight + KV reshard on
-the GPUs of one box.
+the GPUs of one box, in plan order and within the plan's memory budget.
 
 The reference only plans and costs a migration (migration.py:311-384,
 costmodel.py:189-260); the paper's engine executes it with batched async NCCL
-send/recv plus CUDA IPC.  Here every `Transfer` becomes one
-contiguous byte-range copy that the DESTINATION GPU pulls from the source
-GPU's context slab over NVLink (peer-mapped with CUDA IPC, one process per
-GPU), issued by the `k_copy` kernel (`sk_copy_batched`) in plan order; the
-destination's own reusable bytes are copied locally into the new layout.
+send/recv, allocating and releasing migration buffers "based on the migration
+plan".  Here:
+
+* **Memory follows the plan.**  Each GPU's context lives in one arena.  The
+  old shards are placed first; every `Transfer` into the GPU gets a fresh
+  piece of arena when its round starts; at the end of each round the GPU's
+  bytes the plan `releases` (held - kept, migration.py:283-305) go back to the
+  arena's free list and later rounds recycle them.  Kept bytes never move:
+  a new shard is the kept pieces of old shards (aliased in place) plus the
+  received pieces.  So the arena's high-water mark is the plan's
+  `peak_usage` (simulate_buffer_usage, migration.py:387-401) above the old
+  footprint, up to alignment and first-fit fragmentation (`ArenaLayout`,
+  pure host logic, CPU-tested).
+* **Execution follows the plan.**  One persistent `k_exec` launch per rank
+  (include/spotkm.h `sk_exec_plan`) copies 1 MiB chunks in round order over
+  CUDA-IPC peer mappings (NVLink).  A chunk that lands in recycled space
+  waits until every rank has finished the round that freed it -- the only
+  cross-rank dependency -- and the device raises each stage's ready flag as
+  soon as the round its `start_stage` marker follows is globally complete
+  (migration.py:352-371; the paper's per-tensor readiness).
 
 Byte geometry (SURVEY.md finding 8).  A layer's parameters are one flat byte
 array of `bytes_per_layer` bytes; tensor shard [lo, hi) owns bytes
-[lo*B, hi*B) of it.  A request's KV cache of one layer is one flat array of
+[lo*B, hi*B).  A request's KV cache of one layer is one flat array of
 kv_bytes_per_token_per_layer * tokens bytes laid out [head][K|V][tok][hd], so
-a head-fraction shard [lo, hi) is again the contiguous byte range [lo*X, hi*X).
-Every shard boundary must therefore be a whole number of 8-byte words (checked).
+a head-fraction shard [lo, hi) is again the contiguous range [lo*X, hi*X).
+Every shard boundary must be a whole number of 8-byte words (checked).
 """
 
 from __future__ import annotations
@@ -30,7 +45,10 @@ import torch
 from . import _native as nat
 
 CHUNK = 1 << 20          # copy granularity: 1 MiB pieces keep every CTA busy
-ALIGN = 256
+ALIGN = 256              # arena allocation alignment
+EXEC_CHUNK = np.dtype([("src", "<u8"), ("dst", "<u8"), ("bytes", "<u8"), ("round", "<i4"),
+                       ("wait_round", "<i4")])
+assert EXEC_CHUNK.itemsize == 32
 
 
 def _mix64(z: int) -> int:
@@ -49,16 +67,6 @@ def cache_key(seed: int, rid_index: int, layer: int) -> int:
     return _mix64((seed << 20) ^ (2 << 60) ^ (rid_index << 24) ^ layer)
 
 
-@dataclass
-class Slab:
-    """Byte layout of one GPU's context: regions in inventory order."""
-
-    model: dict = field(default_factory=dict)   # layer -> [(lo, hi, where)]  (lo, hi: Fractions)
-    cache: dict = field(default_factory=dict)   # (rid, layer) -> [(lo, hi, tokens, where)]
-    regions: list = field(default_factory=list)  # (where, bytes, key, base); where = (space, offset)
-    bytes: int = 0
-
-
 def _span(frac: Fraction, total: int) -> int:
     v = frac * total
     if v.denominator != 1 or v.numerator % 8:
@@ -66,128 +74,304 @@ def _span(frac: Fraction, total: int) -> int:
     return v.numerator
 
 
-def build_slab(inv, model, rid_index: dict, seed: int, reuse: "Slab | None" = None) -> Slab:
-    """Offsets of an inventory's shards.  With `reuse` (the same GPU's old
-    slab), a shard contained in one the GPU already holds is aliased in place
-    (("old", offset): no allocation, no copy); everything else gets space in
-    the new slab (("new", offset))."""
-    s = Slab()
-    off = 0
-    B, kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
-    for layer, lo, hi in inv.model_shards:
-        a, b = _span(lo, B), _span(hi, B)
-        hit = None
-        if reuse is not None:
-            hit = next((e for e in reuse.model.get(layer, ()) if e[0] <= lo and hi <= e[1]), None)
-        where = ("old", hit[2][1] + _span(lo - hit[0], B)) if hit else ("new", off)
-        s.model.setdefault(layer, []).append((lo, hi, where))
-        s.regions.append((where, b - a, model_key(seed, layer), a))
-        if not hit:
-            off += (b - a + ALIGN - 1) // ALIGN * ALIGN
-    for rid, layer, lo, hi, tok in inv.cache_shards:
-        X = kv * tok
-        a, b = _span(lo, X), _span(hi, X)
-        hit = None
-        if reuse is not None:
-            hit = next((e for e in reuse.cache.get((rid, layer), ())
-                        if e[0] <= lo and hi <= e[1] and e[2] == tok), None)
-        where = ("old", hit[3][1] + _span(lo - hit[0], X)) if hit else ("new", off)
-        s.cache.setdefault((rid, layer), []).append((lo, hi, tok, where))
-        s.regions.append((where, b - a, cache_key(seed, rid_index[rid], layer), a))
-        if not hit:
-            off += (b - a + ALIGN - 1) // ALIGN * ALIGN
-    s.bytes = off
-    return s
+def _align(n: int, a: int = ALIGN) -> int:
+    return (n + a - 1) // a * a
 
 
-def _find(entries, lo, hi):
-    for e in entries:
-        if e[0] <= lo and hi <= e[1]:
-            return e
-    return None
+# ---------------------------------------------------------------------------
+# host-side arena layout (pure Python, no GPU)
+
+MIN_EXTENT = 64 << 10    # smallest piece a received transfer is split into
 
 
-def plan_copies(plan, old_layout, new_required, model, seed: int = 1, with_rounds: bool = False):
-    """Per destination GPU: the ordered byte-range copies that realise `plan`
-    (the plan's transfers in plan order, then local reuse).
-    Returns (old slabs, new slabs, {dst gpu: [(src gpu, src_off, dst_off, bytes)]}); with
-    `with_rounds` also {dst gpu: [plan action index per copy]} (-1 = local reuse)."""
-    rids = sorted({r for inv in list(old_layout.values()) + list(new_required.values())
-                   for r, *_ in inv.cache_shards})
-    rid_index = {r: i for i, r in enumerate(rids)}
-    old = {g: build_slab(inv, model, rid_index, seed) for g, inv in old_layout.items()}
-    new = {g: build_slab(inv, model, rid_index, seed, old.get(g)) for g, inv in new_required.items()}
-    B, kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
-    copies: dict = {g: [] for g in new}
-    rounds: dict = {g: [] for g in new}
-    for a_idx, action in enumerate(plan.actions):
-        for t in action.transfers:
-            if t.kind == "model":
-                src = _find(old[t.src].model.get(t.layer, ()), t.lo, t.hi)
-                dst = _find(new[t.dst].model.get(t.layer, ()), t.lo, t.hi)
-                unit = B
+class Arena:
+    """Round-tagged first-fit arena.  Space freed at the end of round d must
+    not be written before every rank has finished round d, so every
+    allocation reports the latest such round it recycles (`wait`, -1 for
+    fresh space).  A received transfer may be placed as several extents
+    (scatter-gather: the new context is piecewise anyway), so freed holes are
+    reused even when no single one is large enough."""
+
+    def __init__(self):
+        self.free: list[list] = []   # [offset, size, round freed] sorted by offset
+        self.top = 0                 # end of the highest allocation
+        self.high = 0
+
+    def alloc_top(self, n: int) -> int:
+        off = _align(self.top)
+        self.top = off + n
+        self.high = max(self.high, self.top)
+        return off
+
+    def _runs(self):
+        """maximal address-contiguous runs of free pieces: (i, j, start, end, wait)"""
+        fr, i = self.free, 0
+        while i < len(fr):
+            j, end, wait = i, fr[i][0] + fr[i][1], fr[i][2]
+            while j + 1 < len(fr) and fr[j + 1][0] == end:
+                j += 1
+                end = fr[j][0] + fr[j][1]
+                wait = max(wait, fr[j][2])
+            yield i, j, fr[i][0], end, wait
+            i = j + 1
+
+    def _take(self, a: int, b: int) -> int:
+        """remove [a, b) from the free list; -> the latest round it recycles"""
+        keep, wait = [], -1
+        for off, size, rnd in self.free:
+            if off + size <= a or off >= b:
+                keep.append([off, size, rnd])
+                continue
+            wait = max(wait, rnd)
+            if off < a:
+                keep.append([off, a - off, rnd])
+            if off + size > b:
+                keep.append([b, off + size - b, rnd])
+        self.free = keep
+        return wait
+
+    def alloc(self, n: int):
+        """-> [(offset, length, wait round)] extents covering n bytes: one
+        first-fit block if a hole holds it, else the holes in address order
+        (>= MIN_EXTENT each, 256-B aligned), then fresh space at the top."""
+        for i, j, a, b, _ in self._runs():
+            s = _align(a)
+            if b - s >= n:
+                return [(s, n, self._take(s, s + n))]
+        out, left = [], n
+        for i, j, a, b, _ in list(self._runs()):
+            s = _align(a)
+            room = (b - s) // ALIGN * ALIGN
+            if room < MIN_EXTENT and not (b == self.top and left <= room + 0):
+                continue
+            take = min(room, left)
+            if b == self.top and left > room:
+                break   # the run ends at the top: extend it below
+            out.append((s, take, self._take(s, s + take)))
+            left -= take
+            if left == 0:
+                return out
+        # the rest at the top, starting inside a free run that touches it
+        start = _align(self.top)
+        for i, j, a, b, _ in self._runs():
+            if b == self.top and _align(a) < start:
+                start = _align(a)
+        w = self._take(start, start + left) if start < self.top else -1
+        self.top = max(self.top, start + left)
+        self.high = max(self.high, self.top)
+        out.append((start, left, w))
+        return out
+
+    def release(self, off: int, n: int, rnd: int):
+        if n <= 0:
+            return
+        self.free.append([off, n, rnd])
+        self.free.sort()
+        # coalesce neighbours freed in the same round
+        out = []
+        for piece in self.free:
+            if out and out[-1][0] + out[-1][1] == piece[0] and out[-1][2] == piece[2]:
+                out[-1][1] += piece[1]
             else:
-                src = _find([e for e in old[t.src].cache.get((t.request, t.layer), ()) if e[2] == t.tokens],
-                            t.lo, t.hi)
-                dst = _find(new[t.dst].cache.get((t.request, t.layer), ()), t.lo, t.hi)
-                unit = kv * t.tokens
-            if src is None or dst is None:
-                raise ValueError(f"transfer {t} does not fit the slab layouts")
-            n = _span(t.hi - t.lo, unit)
-            if n != t.bytes:
-                raise ValueError(f"transfer bytes {t.bytes} != geometry {n}")
-            if dst[-1][0] != "new":
-                raise ValueError(f"transfer {t} targets a shard its destination already holds")
-            copies[t.dst].append((t.src, src[-1][1] + _span(t.lo - src[0], unit),
-                                  dst[-1][1] + _span(t.lo - dst[0], unit), n))
-            rounds[t.dst].append(a_idx)
-    # local reuse: every needed piece the GPU already holds (the plan's "kept" bytes)
-    for g, slab in new.items():
-        have = old.get(g)
-        local = []
-        if have is not None:
-            for layer, ents in slab.model.items():
-                for lo, hi, (space, off) in ents:
-                    if space != "new":
-                        continue   # aliased in place: nothing to move
-                    for olo, ohi, (_, ooff) in have.model.get(layer, ()):
-                        a, b = max(lo, olo), min(hi, ohi)
-                        if b > a:
-                            local.append((g, ooff + _span(a - olo, B), off + _span(a - lo, B),
-                                          _span(b - a, B)))
-            for key, ents in slab.cache.items():
-                for lo, hi, tok, (space, off) in ents:
-                    if space != "new":
-                        continue
-                    for olo, ohi, otok, (_, ooff) in have.cache.get(key, ()):
-                        a, b = max(lo, olo), min(hi, ohi)
-                        if b > a and otok == tok:
-                            X = kv * tok
-                            local.append((g, ooff + _span(a - olo, X), off + _span(a - lo, X),
-                                          _span(b - a, X)))
-        # NVLink pulls first (the scarce link), local reuse copies after them:
-        # the copy kernel's CTAs take chunks in list order, so the local HBM
-        # copies fill in behind the remote traffic instead of delaying it
-        copies[g] = copies[g] + local
-        rounds[g] = rounds[g] + [-1] * len(local)
-    if with_rounds:
-        return old, new, copies, rounds
-    return old, new, copies
+                out.append(piece)
+        self.free = out
 
 
-def issue_lists(copies: dict, owner: dict, mode: str = "pull", rounds: dict | None = None) -> dict:
-    """Which rank issues which copy: pull -> the destination GPU's rank, push ->
-    the source GPU's rank; local (same-GPU) copies always by the owner.
-    Returns {rank: [(src, dst, src_off, dst_off, bytes)]} in plan order (with
-    `rounds`, each entry carries its plan action index as a 6th field)."""
-    out: dict = {}
-    for dst, lst in copies.items():
-        for i, (src, soff, doff, n) in enumerate(lst):
-            issuer = dst if (mode == "pull" or src == dst) else src
-            row = (src, dst, soff, doff, n) if rounds is None else (src, dst, soff, doff, n, rounds[dst][i])
-            out.setdefault(owner[issuer], []).append(row)
-    return out
+@dataclass
+class Region:
+    """One contiguous byte range of a context object held in an arena."""
 
+    key: tuple            # ("m", layer) or ("c", rid, layer)
+    lo: Fraction          # shard interval of the object
+    hi: Fraction
+    tokens: int
+    unit: int             # object bytes per unit interval (B or kv * tokens)
+    off: int              # arena byte offset of lo
+    released: list = field(default_factory=list)   # (round, [lo, hi)) sub-intervals freed
+
+    def byte_range(self, lo: Fraction, hi: Fraction):
+        return self.off + _span(lo - self.lo, self.unit), _span(hi - lo, self.unit)
+
+
+@dataclass
+class GpuLayout:
+    arena: Arena
+    old: list                 # Regions of the old context
+    pieces: list              # new context: (key, lo, hi, tokens, unit, arena offset)
+    incoming: dict            # id(transfer) -> [(arena offset, length, wait round)] extents
+    old_bytes: int            # exact bytes of the old context
+    old_footprint: int        # arena bytes after placing it (aligned)
+
+
+class ArenaLayout:
+    """Where every byte of a plan's old and new contexts lives, per GPU, and
+    which arena space each transfer recycles (see the module docstring).
+
+    `rounds`: the plan's non-start_stage actions in order (round index =
+    position); `stage_round[stage]` = the last round before its marker (-1:
+    ready at the start)."""
+
+    def __init__(self, plan, old_layout, new_required, model, recycle: bool = True):
+        self.plan = plan
+        self.recycle = recycle
+        self.B, self.kv = model.bytes_per_layer, model.kv_bytes_per_token_per_layer
+        self.rounds = [a for a in plan.actions if a.kind != "start_stage"]
+        self.stage_round = {}
+        r = -1
+        for a in plan.actions:
+            if a.kind == "start_stage":
+                self.stage_round[a.stage] = r
+            else:
+                r += 1
+        gpus = sorted(set(old_layout) | set(new_required))
+        self.gpus: dict = {}
+        for g in gpus:
+            self.gpus[g] = self._place_old(old_layout.get(g))
+        # per round: allocate the incoming pieces, then free the releases
+        need = {g: new_required.get(g) for g in gpus}
+        kept = {g: self._kept(self.gpus[g].old, need[g]) for g in gpus}
+        self.freed_bytes: list[dict] = []
+        for ri, action in enumerate(self.rounds):
+            for t in action.transfers:
+                gl = self.gpus[t.dst]
+                unit = self.B if t.kind == "model" else self.kv * t.tokens
+                n = _span(t.hi - t.lo, unit)
+                if n != t.bytes:
+                    raise ValueError(f"transfer bytes {t.bytes} != geometry {n}")
+                ext = gl.arena.alloc(n)
+                gl.incoming[id(t)] = ext
+                key = ("m", t.layer) if t.kind == "model" else ("c", t.request, t.layer)
+                pos = 0
+                for off, ln, _ in ext:
+                    lo = t.lo + Fraction(pos, unit)
+                    gl.pieces.append((key, lo, lo + Fraction(ln, unit), t.tokens, unit, off))
+                    pos += ln
+            self.freed_bytes.append(self._release(ri, action, kept))
+        for g in gpus:
+            gl = self.gpus[g]
+            for reg in gl.old:
+                for lo, hi in kept[g].get(id(reg), ()):
+                    gl.pieces.append((reg.key, lo, hi, reg.tokens, reg.unit, reg.byte_range(lo, hi)[0]))
+            self._check_coverage(g, need[g])
+
+    def _place_old(self, inv):
+        ar = Arena()
+        regs = []
+        total = 0
+        if inv is not None:
+            for layer, lo, hi in inv.model_shards:
+                n = _span(hi - lo, self.B)
+                regs.append(Region(("m", layer), lo, hi, 0, self.B, ar.alloc_top(n)))
+                total += n
+            for rid, layer, lo, hi, tok in inv.cache_shards:
+                n = _span(hi - lo, self.kv * tok)
+                regs.append(Region(("c", rid, layer), lo, hi, tok, self.kv * tok, ar.alloc_top(n)))
+                total += n
+        return GpuLayout(ar, regs, [], {}, total, _align(ar.top))
+
+    @staticmethod
+    def _kept(regs, need):
+        """id(region) -> [(lo, hi)] of it the GPU keeps for its own new context
+        (the `kept` of migration.py:287-303)."""
+        out: dict = {}
+        if need is None:
+            return out
+        want: dict = {}
+        for layer, lo, hi in need.model_shards:
+            want.setdefault(("m", layer), []).append((lo, hi, 0))
+        for rid, layer, lo, hi, tok in need.cache_shards:
+            want.setdefault(("c", rid, layer), []).append((lo, hi, tok))
+        for reg in regs:
+            for lo, hi, tok in want.get(reg.key, ()):
+                a, b = max(lo, reg.lo), min(hi, reg.hi)
+                if b <= a:
+                    continue
+                if reg.key[0] == "c" and tok != reg.tokens:
+                    raise ValueError("kept KV shard with a different token count: the byte-range "
+                                     "executor keeps whole per-token blocks only")
+                out.setdefault(id(reg), []).append((a, b))
+        return out
+
+    def _release(self, ri, action, kept):
+        """Free, at the end of round ri, every old byte the plan releases in
+        it: held - kept of the round's layer (migrate_layer) or of all cache
+        shards (migrate_cache).  Returns {instance: bytes freed} for the
+        cross-check against the plan's `releases`."""
+        freed: dict = {}
+        for g, gl in self.gpus.items():
+            for reg in gl.old:
+                if action.kind == "migrate_layer" and reg.key != ("m", action.layer):
+                    continue
+                if action.kind == "migrate_cache" and reg.key[0] != "c":
+                    continue
+                pieces = [(reg.lo, reg.hi)]
+                for a, b in sorted(kept[g].get(id(reg), ())):
+                    nxt = []
+                    for lo, hi in pieces:
+                        if b <= lo or a >= hi:
+                            nxt.append((lo, hi))
+                            continue
+                        if lo < a:
+                            nxt.append((lo, a))
+                        if b < hi:
+                            nxt.append((b, hi))
+                    pieces = nxt
+                for lo, hi in pieces:
+                    off, n = reg.byte_range(lo, hi)
+                    if self.recycle:
+                        gl.arena.release(off, n, ri)
+                    reg.released.append((ri, lo, hi))
+                    freed[g[0]] = freed.get(g[0], 0) + n
+        return freed
+
+    def _check_coverage(self, g, need):
+        have: dict = {}
+        for key, lo, hi, tok, unit, off in self.gpus[g].pieces:
+            have.setdefault(key, []).append((lo, hi))
+        want = []
+        if need is not None:
+            want = [(("m", layer), lo, hi) for layer, lo, hi in need.model_shards]
+            want += [(("c", rid, layer), lo, hi) for rid, layer, lo, hi, tok in need.cache_shards]
+        for key, lo, hi in want:
+            ps = sorted(have.get(key, ()))
+            pos = lo
+            for a, b in ps:
+                if a <= pos < b:
+                    pos = b
+            if pos < hi:
+                raise ValueError(f"new context of {g} misses {key} [{pos}, {hi})")
+
+    # -- reports -------------------------------------------------------------
+    def check_releases(self):
+        """Bytes the arena frees per round and instance == the plan's
+        `releases` (relative 1e-12: the plan sums per-shard floats)."""
+        for ri, action in enumerate(self.rounds):
+            plan_rel = dict(action.releases)
+            mine = self.freed_bytes[ri]
+            if set(plan_rel) != set(mine):
+                raise ValueError(f"round {ri}: released instances {sorted(mine)} != plan {sorted(plan_rel)}")
+            for inst, b in plan_rel.items():
+                if abs(mine[inst] - b) > 1e-12 * max(1.0, b):
+                    raise ValueError(f"round {ri}: {inst} frees {mine[inst]} != plan {b}")
+
+    def memory_report(self):
+        """Per instance: old footprint, arena high-water, and the plan's
+        peak_usage (migration buffers above the old context)."""
+        per_inst: dict = {}
+        for g, gl in self.gpus.items():
+            d = per_inst.setdefault(g[0], {"old_bytes": 0, "arena_bytes": 0})
+            d["old_bytes"] += gl.old_bytes
+            d["arena_bytes"] += gl.arena.high
+        for inst, d in per_inst.items():
+            peak = float(self.plan.peak_usage.get(inst, 0.0))
+            d["plan_peak_usage"] = peak
+            d["plan_bound_bytes"] = d["old_bytes"] + peak
+            d["arena_over_plan"] = d["arena_bytes"] / max(1.0, d["old_bytes"] + peak)
+        return per_inst
+
+
+# ---------------------------------------------------------------------------
+# device side
 
 def traffic(plan):
     """bytes in / out per GPU over NVLink (src != dst GPU)."""
@@ -214,154 +398,281 @@ class _Mem:
             self.ptr = None
 
 
-class ReshardExecutor:
-    """Executes one plan on this process's GPU(s).
+def _exec_lib():
+    lib = nat.load()
+    if not getattr(lib, "_exec_sigs", False):
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        lib.sk_exec_ctl_bytes.argtypes = [i32, i32]
+        lib.sk_exec_ctl_bytes.restype = i64
+        lib.sk_exec_plan.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, i32, i32, ctypes.c_double, vp]
+        lib.sk_exec_plan.restype = i32
+        lib.sk_memcpy_batched.argtypes = [vp, i32, vp]
+        lib.sk_memcpy_batched.restype = i32
+        lib.sk_d2h.argtypes = [vp, vp, ctypes.c_uint64]
+        lib.sk_d2h.restype = i32
+        lib._exec_sigs = True
+    return lib
 
-    `owner[gpu_ref]` = rank hosting that GPU.  With one process per GPU the
-    ranks exchange CUDA IPC handles of their old-context slabs through
-    torch.distributed (gloo/nccl object all-gather) and each destination pulls
-    from peers over NVLink.  With world == 1 every GPU ref is emulated on the
-    local device (same code path, local pointers) -- used by the tests.
+
+def slab_offsets(layout: "ArenaLayout", owner: dict, rank: int, ctl_bytes: int):
+    """This rank's slab: [control block | arena(ref) ...] -> ({ref: offset}, size)."""
+    off = _align(ctl_bytes)
+    ref_off = {}
+    for g in sorted(g for g, r in owner.items() if r == rank):
+        ref_off[g] = off
+        if g in layout.gpus:
+            off = _align(off + layout.gpus[g].arena.high)
+    return ref_off, off
+
+
+def exchange_slabs(rank: int, world: int, slab_ptr: int, handle: bytes, ref_off: dict, opener, group=None):
+    """All-gather every rank's (IPC handle, arena offsets) and map the peers'
+    slabs with `opener(handle) -> device pointer`.  Returns ({ref: arena base
+    usable here}, {rank: control block pointer usable here}, [opened ptrs])."""
+    base = {g: slab_ptr + o for g, o in ref_off.items()}
+    ctl = {rank: slab_ptr}
+    opened = []
+    if world > 1:
+        import torch.distributed as dist
+
+        gathered = [None] * world
+        dist.all_gather_object(gathered, {"handle": handle, "ref_off": ref_off}, group=group)
+        for r, doc in enumerate(gathered):
+            if r == rank:
+                continue
+            p = opener(doc["handle"])
+            opened.append(p)
+            ctl[r] = p
+            for g, o in doc["ref_off"].items():
+                base[g] = p + o
+    return base, ctl, opened
+
+
+def region_of(layout: "ArenaLayout", g, t) -> Region:
+    """The old shard of GPU g a transfer reads from."""
+    key = ("m", t.layer) if t.kind == "model" else ("c", t.request, t.layer)
+    for reg in layout.gpus[g].old:
+        if reg.key == key and reg.lo <= t.lo and t.hi <= reg.hi and (t.kind == "model" or reg.tokens == t.tokens):
+            return reg
+    raise ValueError(f"transfer {t} has no source shard on {g}")
+
+
+def issue_list(layout: "ArenaLayout", owner: dict, rank: int, mode: str, base: dict):
+    """The copies `rank` issues, in plan order: pull -> the transfers into its
+    GPUs, push -> the transfers out of them.  One entry per received extent:
+    (round, src ptr, dst ptr, bytes, wait round, transfer)."""
+    out = []
+    for ri, action in enumerate(layout.rounds):
+        for t in action.transfers:
+            if owner[t.dst if mode == "pull" else t.src] != rank:
+                continue
+            s_off, _ = region_of(layout, t.src, t).byte_range(t.lo, t.hi)
+            pos = 0
+            for d_off, ln, w in layout.gpus[t.dst].incoming[id(t)]:
+                out.append((ri, base[t.src] + s_off + pos, base[t.dst] + d_off, ln, w, t))
+                pos += ln
+    return out
+
+
+def p2p_ops(layout: "ArenaLayout", owner: dict, rank: int, local_base: dict):
+    """`rank`'s side of every transfer extent, in plan order, for a send/recv
+    baseline: ("send", peer, local ptr, n), ("recv", peer, local ptr, n), or
+    ("local", None, (src, dst), n) when both GPUs are this rank's.  Matching
+    send/recv pairs appear in the same order on both ranks."""
+    out = []
+    for action in layout.rounds:
+        for t in action.transfers:
+            rs, rd = owner[t.src], owner[t.dst]
+            if rank not in (rs, rd):
+                continue
+            s_off, _ = region_of(layout, t.src, t).byte_range(t.lo, t.hi)
+            pos = 0
+            for d_off, ln, _ in layout.gpus[t.dst].incoming[id(t)]:
+                if rs == rd:
+                    out.append(("local", None, (local_base[t.src] + s_off + pos, local_base[t.dst] + d_off), ln))
+                elif rs == rank:
+                    out.append(("send", rd, local_base[t.src] + s_off + pos, ln))
+                else:
+                    out.append(("recv", rs, local_base[t.dst] + d_off, ln))
+                pos += ln
+    return out
+
+
+class ReshardExecutor:
+    """Executes one MigrationPlan on this process's GPU(s).
+
+    `owner[gpu_ref]` = rank hosting that GPU.  Each rank allocates ONE slab
+    (control block + one arena per owned GPU ref, sized by ArenaLayout), the
+    ranks exchange CUDA IPC handles of their slabs through torch.distributed,
+    and each rank's k_exec launch issues its share of the copies: pull = the
+    transfers INTO its GPUs (reading peers' old shards over NVLink), push =
+    the transfers OUT of its GPUs.  With world == 1 every GPU ref is emulated
+    in the local slab (same code path, local pointers) -- used by the tests.
+    `recycle=False` keeps released bytes allocated (arena = old + every
+    received byte): the layout the order-free comparison paths
+    (run_unordered, run_memcpy, NCCL) need.
     """
 
     def __init__(self, plan, old_layout, new_required, model, owner: dict, rank: int = 0,
-                 world: int = 1, seed: int = 1, group=None, mode: str = "pull", chunk: int = CHUNK):
+                 world: int = 1, seed: int = 1, group=None, mode: str = "pull", chunk: int = CHUNK,
+                 timeout_s: float = 30.0, recycle: bool = True):
         if mode not in ("pull", "push"):
             raise ValueError("mode must be 'pull' or 'push'")
-        self.lib = nat.load()
-        self.rank, self.world, self.mode = rank, world, mode
-        self.old, self.new, copies, rounds = plan_copies(plan, old_layout, new_required, model, seed,
-                                                         with_rounds=True)
+        self.lib = _exec_lib()
+        self.rank, self.world, self.mode, self.group = rank, world, mode, group
         self.plan = plan
-        self.mine = [g for g, r in owner.items() if r == rank]
-        self.old_mem = {g: _Mem(self.old[g].bytes) for g in self.mine if g in self.old}
-        self.new_mem = {g: _Mem(self.new[g].bytes) for g in self.mine if g in self.new}
-        # device addresses usable from this GPU: own slabs + peer-mapped slabs
-        self.old_ptr = {g: m.ptr for g, m in self.old_mem.items()}
-        self.new_ptr = {g: m.ptr for g, m in self.new_mem.items()}
-        self.opened = []
+        self.timeout_s = timeout_s
+        self.layout = ArenaLayout(plan, old_layout, new_required, model, recycle)
+        self.layout.check_releases()
+        L = self.layout
+        self.n_rounds = len(L.rounds)
+        stages = sorted(L.stage_round)
+        self.stages = stages
+        self.ctl_bytes = int(self.lib.sk_exec_ctl_bytes(self.n_rounds, len(stages)))
+        # this rank's slab: [control | arena(ref) ...], peers' slabs IPC-mapped
+        self.mine = sorted(g for g, r in owner.items() if r == rank)
+        ref_off, size = slab_offsets(L, owner, rank, self.ctl_bytes)
+        self.slab = _Mem(size)
+        handle = b""
         if world > 1:
-            import torch.distributed as dist
+            h = ctypes.create_string_buffer(64)
+            nat.check(self.lib.sk_ipc_get_handle(self.slab.ptr, h))
+            handle = h.raw
 
-            handles = {}
-            for tag, mems in (("old", self.old_mem), ("new", self.new_mem)):
-                for g, m in mems.items():
-                    h = ctypes.create_string_buffer(64)
-                    nat.check(self.lib.sk_ipc_get_handle(m.ptr, h))
-                    handles[(tag, g)] = h.raw
-            gathered = [None] * world
-            dist.all_gather_object(gathered, handles, group=group)
-            for r, hs in enumerate(gathered):
-                if r == rank:
-                    continue
-                for (tag, g), raw in hs.items():
-                    if (tag == "old") != (mode == "pull"):
-                        continue   # pull maps peers' old slabs, push their new slabs
-                    p = ctypes.c_void_p()
-                    nat.check(self.lib.sk_ipc_open_handle(raw, ctypes.byref(p)))
-                    (self.old_ptr if tag == "old" else self.new_ptr)[g] = p.value
-                    self.opened.append(p.value)
-        self.peer_ptr = self.old_ptr
+        def opener(raw):
+            p = ctypes.c_void_p()
+            nat.check(self.lib.sk_ipc_open_handle(raw, ctypes.byref(p)))
+            return p.value
+
+        base, ctl_ptr, self.opened = exchange_slabs(rank, world, self.slab.ptr, handle, ref_off, opener, group)
+        self.base = base
+        self.owner = owner
+        self.local_base = {g: self.slab.ptr + o for g, o in ref_off.items()}
         dev = torch.device("cuda", torch.cuda.current_device())
-        self._issued = issue_lists(copies, owner, mode, rounds).get(rank, ())
         self._dev = dev
-        self.local_bytes = sum(n for src, dst, _, _, n, _ in self._issued if src == dst)
-        self.remote_bytes = sum(n for src, dst, _, _, n, _ in self._issued if src != dst)
-        self.set_chunk(chunk)
-        self.d_fill = self._regions(self.old, self.old_mem, self.old_mem, dev)
-        self.d_check = self._regions(self.new, self.new_mem, self.old_mem, dev)
+        # the copies this rank issues, in plan order, cut into chunks
+        rows, rnd, wait = [], [], []
+        self.transfers_issued = []
+        issued = issue_list(L, owner, rank, mode, base)
+        for ri, src_ptr, dst_ptr, ln, w, t in issued:
+            self.transfers_issued.append((src_ptr, dst_ptr, ln, owner[t.src], owner[t.dst]))
+            for c in range(0, ln, chunk):
+                rows.append((src_ptr + c, dst_ptr + c, min(chunk, ln - c)))
+                rnd.append(ri)
+                wait.append(w)
+        self.remote_bytes = sum(e[3] for e in issued)
+        ch = np.zeros(len(rows), dtype=EXEC_CHUNK)
+        if rows:
+            arr = np.array(rows, dtype=np.uint64)
+            ch["src"], ch["dst"], ch["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
+            ch["round"], ch["wait_round"] = rnd, wait
+        self.n_chunks = len(ch)
+        totals = np.bincount(np.array(rnd, dtype=np.int64), minlength=self.n_rounds).astype(np.uint32) \
+            if rnd else np.zeros(self.n_rounds, np.uint32)
+        srounds = np.array([L.stage_round[s] for s in stages], dtype=np.int32)
+        peers = [ctl_ptr[r] + 4 for r in sorted(ctl_ptr) if r != rank]
+        self.d_chunks = torch.from_numpy(ch.view(np.uint8)).to(dev) if len(ch) else None
+        self.d_totals = torch.from_numpy(np.ascontiguousarray(totals).view(np.uint8)).to(dev) \
+            if self.n_rounds else None
+        self.d_stages = torch.from_numpy(srounds.view(np.uint8)).to(dev) if len(stages) else None
+        self.d_peers = torch.from_numpy(np.array(peers or [0], dtype=np.uint64).view(np.uint8)).to(dev)
+        self.n_peers = len(peers)
+        # unordered one-launch copy list (k_copy) and per-transfer copy list (copy engines)
+        cp = np.zeros(len(rows), dtype=nat.COPY)
+        if rows:
+            cp["src"], cp["dst"], cp["bytes"] = ch["src"], ch["dst"], ch["bytes"]
+        self.d_copies = torch.from_numpy(cp.view(np.uint8)).to(dev) if len(cp) else None
+        tr = np.zeros(len(self.transfers_issued), dtype=nat.COPY)
+        for i, (s, d, n, _, _) in enumerate(self.transfers_issued):
+            tr[i] = (s, d, n)
+        self.h_transfers = tr
+        self.d_fill = self._regions(seed, new=False)
+        self.d_check = self._regions(seed, new=True)
         self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
 
-    def set_chunk(self, chunk: int = CHUNK):
-        """(Re)build the device copy lists with `chunk`-byte pieces."""
-        rows, rnd = [], []
-        for src, dst, soff, doff, n, r in self._issued:
-            sbase, dbase = self.old_ptr[src], self.new_ptr[dst]
-            for c in range(0, n, chunk):
-                rows.append((sbase + soff + c, dbase + doff + c, min(chunk, n - c)))
-                rnd.append(r)
+    def _regions(self, seed, new: bool):
+        rids = sorted({k[1] for gl in self.layout.gpus.values() for r in gl.old for k in [r.key] if k[0] == "c"}
+                      | {p[0][1] for gl in self.layout.gpus.values() for p in gl.pieces if p[0][0] == "c"})
+        rid_index = {r: i for i, r in enumerate(rids)}
 
-        def to_dev(rs):
-            arr = np.array(rs, dtype=np.uint64).reshape(-1, 3) if rs else np.zeros((0, 3), np.uint64)
-            cp = np.zeros(len(arr), dtype=nat.COPY)
-            if len(arr):
-                cp["src"], cp["dst"], cp["bytes"] = arr[:, 0], arr[:, 1], arr[:, 2]
-            return (torch.from_numpy(cp.view(np.uint8)).to(self._dev) if len(cp) else None), len(cp)
+        def key_of(key):
+            return model_key(seed, key[1]) if key[0] == "m" else cache_key(seed, rid_index[key[1]], key[2])
 
-        # one-launch order: NVLink transfers in plan order, local reuse last
-        self.d_copies, self.n_copies = to_dev(rows)
-        # progressive order: local reuse first, then round by round
-        order = sorted(range(len(rows)), key=lambda i: (rnd[i], i))
-        self.d_prog, _ = to_dev([rows[i] for i in order])
-        ro = [rnd[i] for i in order]
-        self.round_ranges = []   # (action index, begin, end) in the progressive array
-        i = 0
-        while i < len(ro):
-            j = i
-            while j < len(ro) and ro[j] == ro[i]:
-                j += 1
-            self.round_ranges.append((ro[i], i, j))
-            i = j
-
-    @staticmethod
-    def _regions(slabs, mems, old_mems, dev):
         rows = []
-        for g, m in mems.items():
-            for where, n, key, base in slabs[g].regions:
-                space, off = where
-                ptr = (m.ptr if space == "new" else old_mems[g].ptr) + off
-                rows.append((ptr, n, key, base))
+        for g in self.mine:
+            gl = self.layout.gpus.get(g)
+            if gl is None:
+                continue
+            if new:
+                for key, lo, hi, tok, unit, off in gl.pieces:
+                    rows.append((self.base[g] + off, _span(hi - lo, unit), key_of(key), _span(lo, unit)))
+            else:
+                for reg in gl.old:
+                    rows.append((self.base[g] + reg.off, _span(reg.hi - reg.lo, reg.unit), key_of(reg.key),
+                                 _span(reg.lo, reg.unit)))
         reg = np.zeros(len(rows), dtype=nat.REGION)
         for i, r in enumerate(rows):
             reg[i] = r
-        return (torch.from_numpy(reg.view(np.uint8)).to(dev), len(rows)) if rows else (None, 0)
+        return (torch.from_numpy(reg.view(np.uint8)).to(self._dev), len(rows)) if rows else (None, 0)
 
+    # -- running -------------------------------------------------------------
     def fill_old(self):
+        """(Re)write every old shard's pattern -- needed before each run, since
+        a run recycles released old space for received data."""
         t, n = self.d_fill
         if n:
             nat.check(self.lib.sk_fill_regions(t.data_ptr(), n, torch.cuda.current_stream().cuda_stream))
 
     def run(self, n_ctas: int = 0):
-        """The reshard: one launch of k_copy over this rank's copies, in plan order."""
-        if self.n_copies:
-            nat.check(self.lib.sk_copy_batched(self.d_copies.data_ptr(), self.n_copies, n_ctas,
+        """The reshard: one k_exec launch over this rank's copies, in plan
+        order (resets the control block first; ranks must barrier between
+        runs so no peer reads a stale progress word)."""
+        st = torch.cuda.current_stream().cuda_stream
+        nat.check(self.lib.sk_exec_plan(
+            self.d_chunks.data_ptr() if self.d_chunks is not None else 0, self.n_chunks,
+            self.d_totals.data_ptr() if self.d_totals is not None else 0, self.n_rounds,
+            self.d_stages.data_ptr() if self.d_stages is not None else 0, len(self.stages),
+            self.slab.ptr, self.d_peers.data_ptr(), self.n_peers, n_ctas, self.timeout_s, st))
+
+    def run_unordered(self, n_ctas: int = 0):
+        """Data path only: the same chunks in one k_copy launch with no round
+        order or recycling waits (for NVLink counters; byte-exact only with
+        recycle=False)."""
+        if self.d_copies is not None:
+            nat.check(self.lib.sk_copy_batched(self.d_copies.data_ptr(), self.n_chunks, n_ctas,
                                                torch.cuda.current_stream().cuda_stream))
 
-    def run_progressive(self, n_ctas: int = 0) -> dict:
-        """Round-by-round execution with a CUDA event per plan round, so a
-        stage can start serving as soon as the round its `start_stage` marker
-        follows has landed (PAPER.md:497's per-tensor readiness; the marker
-        placement is migration.py:352-371).  Returns {stage: event} recorded on
-        the current stream: this rank's copies for every round up to that
-        marker are complete when the event fires."""
-        st = torch.cuda.current_stream()
-        begin = torch.cuda.Event(enable_timing=True)
-        begin.record(st)
-        ptr = self.d_prog.data_ptr() if self.d_prog is not None else 0
-        ranges = {r: (b, e) for r, b, e in self.round_ranges}
+    def run_memcpy(self):
+        """Copy-engine comparison: one cudaMemcpyAsync per issued transfer
+        extent, in plan order on the current stream (no recycling waits
+        either: byte-exact only with recycle=False)."""
+        if len(self.h_transfers):
+            nat.check(self.lib.sk_memcpy_batched(self.h_transfers.ctypes.data, len(self.h_transfers),
+                                                 torch.cuda.current_stream().cuda_stream))
 
-        def launch(r):
-            b, e = ranges[r]
-            nat.check(self.lib.sk_copy_batched(ptr + 24 * b, e - b, n_ctas, st.cuda_stream))
+    def p2p_ops(self):
+        """This rank's side of every transfer extent for a send/recv baseline
+        (see `p2p_ops`)."""
+        return p2p_ops(self.layout, self.owner, self.rank, self.local_base)
 
-        if -1 in ranges:
-            launch(-1)  # local reuse first (HBM only)
-        last = torch.cuda.Event(enable_timing=True)
-        last.record(st)
-        ready = {}
-        for idx, action in enumerate(self.plan.actions):
-            if action.kind == "start_stage":
-                ready[action.stage] = last
-                continue
-            if idx in ranges:
-                launch(idx)
-            last = torch.cuda.Event(enable_timing=True)
-            last.record(st)
-        self.progress_begin = begin
-        return ready
+    def control(self) -> dict:
+        """This rank's control block after a run (synchronizes): error code,
+        rounds completed, stage flags and stage-ready times (ms after launch)."""
+        torch.cuda.synchronize()
+        raw = np.zeros(self.ctl_bytes, dtype=np.uint8)
+        nat.check(self.lib.sk_d2h(raw.ctypes.data, self.slab.ptr, self.ctl_bytes))
+        w = raw.view(np.uint32)
+        R, S = self.n_rounds, len(self.stages)
+        flags = w[4 + R:4 + R + S]
+        so = ((4 + R + S + 1) & ~1) * 4
+        stamps = raw[so:so + 8 * (S + 1)].view(np.uint64).astype(np.float64)
+        return {"error": int(w[2]), "progress": int(w[1]), "rounds": R,
+                "stage_flags": {s: int(f) for s, f in zip(self.stages, flags)},
+                "stage_ready_ms": {s: (stamps[1 + i] - stamps[0]) / 1e6 for i, s in enumerate(self.stages)}}
 
     def verify(self) -> int:
-        """Mismatching 8-byte words in this rank's new slabs (0 = byte-identical)."""
+        """Mismatching 8-byte words in this rank's new contexts (0 = every
+        required shard byte-identical, kept and received pieces alike)."""
         t, n = self.d_check
         self.d_bad.zero_()
         if n:
@@ -381,9 +692,8 @@ class ReshardExecutor:
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.barrier(group=group)
-        for m in list(self.old_mem.values()) + list(self.new_mem.values()):
-            m.free()
+            dist.barrier(group=group if group is not None else self.group)
+        self.slab.free()
 
 
 def required_layout(mapping, model, inherited_by_pipeline=None, inventory_cls=None):
@@ -411,13 +721,17 @@ def common_k(*layouts) -> int:
 
 GPT20B_BF16 = ("gpt-20b-bf16", 44, 12 * 6144 * 6144 * 2, 2 * 6144 * 2)
 LLAMA30B_BF16 = ("llama-30b-bf16", 60, (4 * 6656 * 6656 + 3 * 6656 * 17920) * 2, 2 * 6656 * 2)
+U_MAX = 4e9   # the B_S scenario's migration buffer cap (data/scenario_bs.json:14)
 
 
-def make_reshard_problem(geom, old_shape, new_shape, batch: int = 8, seq: int = 2048):
+def make_reshard_problem(geom, old_shape, new_shape, batch: int = 8, seq: int = 2048,
+                         u_max: float | None = U_MAX, mapper=None):
     """One GPU per instance (G=1), old config laid out positionally on i-0..i-(N-1),
     `batch` cached requests of `seq` tokens per old pipeline, identity
     inheritance.  The mapping and plan come from this package's device mapper
-    and native planner.  Returns (plan, old_layout, new_required, model, refs)."""
+    (or `mapper`, same signature) and native planner (memory-optimised layer
+    order under `u_max`).
+    Returns (plan, old_layout, new_required, model, refs)."""
     from . import domain as dm
     from .mapping import default_inheritance, map_devices
     from .planner import plan_migration
@@ -444,9 +758,9 @@ def make_reshard_problem(geom, old_shape, new_shape, batch: int = 8, seq: int = 
         layout[ref] = inv
         insts.append(dm.InstanceState(id=f"i-{k}", kind="spot", gpus=1, gpu_inventories=[inv]))
     inh = default_inheritance(old.data_parallel, new.data_parallel)
-    mapping = map_devices(insts, new, model, 1, inheritance=inh, requests_by_old_pipeline=reqs)
+    mapping = (mapper or map_devices)(insts, new, model, 1, inheritance=inh, requests_by_old_pipeline=reqs)
     inherited = {inh[d]: [(r.id, seq) for r in reqs[d]] for d in sorted(reqs) if d in inh}
-    plan = plan_migration(mapping, layout, model, inherited_by_pipeline=inherited)
+    plan = plan_migration(mapping, layout, model, u_max=u_max, inherited_by_pipeline=inherited)
     need = required_layout(mapping, model, inherited, dm.ContextInventory)
     for ref in layout:
         need.setdefault(ref, dm.ContextInventory())

@@ -50,3 +50,25 @@ def own_from_port(instances, new, G, inh, reqs, model_geom):
     rq = {d: [sk.RequestSpec(id=rid, arrival_time=0.0, s_in=tok, s_out=max(tok, 1)) for rid, tok in lst]
           for d, lst in reqs.items()}
     return mspec, sk.ParallelConfig(*new, 1), insts, rq
+
+
+def port_mapper(instances, target, model, G, inheritance=None, requests_by_old_pipeline=None,
+                fused_weight="max"):
+    """map_devices computed by the CPU oracle (tests only: lets host-side
+    executor logic be tested without a GPU)."""
+    from oracle import port
+
+    insts = sorted(instances, key=lambda i: natural_key(i.id))
+    pinst = [(i.id, [port.Inv(tuple(v.model_shards), tuple(v.cache_shards)) for v in i.gpu_inventories])
+             for i in insts]
+    reqs = None
+    if requests_by_old_pipeline is not None:
+        reqs = {d: [(r.id, r.s_in + r.tokens_generated) for r in rs]
+                for d, rs in requests_by_old_pipeline.items()}
+    tgt = (target.data_parallel, target.pipeline_stages, target.tensor_shards)
+    refs, slots, W, assign, total = port.map_devices(pinst, tgt, (model.num_layers, model.bytes_per_layer,
+                                                                  model.kv_bytes_per_token_per_layer),
+                                                     G, inheritance, reqs, fused_weight)
+    pos = sk.positions(target)
+    mapping = {refs[r]: pos[c] for r, c in enumerate(assign) if c >= 0}
+    return sk.DeviceMapping(assignment=mapping, total_weight=total, config=target)

@@ -75,6 +75,12 @@ def _ref_plan(q):
     return q, cols, total.hex(), time.perf_counter() - t0
 
 
+def _warm(_):
+    import oracle.sweep_inputs  # noqa: F401
+
+    return os.getpid()
+
+
 def sample_order(n_plans: int, n_pairs: int = 36):
     """Plans round-robin over the config pairs (the batch is sorted by outer
     size, so consecutive indices are one size class)."""
@@ -96,7 +102,7 @@ def cpu_reference_rate(batch, model, seconds: float, cores: int, spot, order=Non
     answers = {}
     with ProcessPoolExecutor(max_workers=cores, mp_context=ctx) as ex:
         # warm the workers (imports, first-call costs) outside the window
-        list(ex.map(os.getpid, range(cores)))
+        list(ex.map(_warm, range(cores)))
         it = iter(order)
         t0 = time.perf_counter()
         running = set()
@@ -170,7 +176,7 @@ def _spot_plan_inputs(doc, spot):
 
 def config1_problems(ns, map_devices, required_context_with_cache):
     """BASELINE.json configs[0]: GPT-20B (2,2,8) on 12 four-GPU instances
-    (positional on i-0..i-7, 8 cached requests of 512 + 128 tokens per
+    (positional on i-0..i-7, 8 cached requests of 512 + 64 tokens per
     pipeline), replanned to (1,2,8) and then to (2,3,4).  `ns` is the domain
     namespace (the reference's or this package's); returns the two
     map_devices argument tuples (the second one's layout is the first
@@ -272,7 +278,9 @@ def dropin_block(spot, ref_reps: int = 1):
             sa = ref_c1[k]
             m = spot.mapping.map_devices(*sa[:4], inheritance=sa[4], requests_by_old_pipeline=sa[5],
                                          fused_weight=sa[6])
-            r["exact_vs_reference"] = (assignment_cols(got, insts, cfg) == assignment_cols(m, sa[0], sa[1])
+            from oracle.sweep_inputs import mapping_cols
+
+            r["exact_vs_reference"] = (assignment_cols(got, insts, cfg) == mapping_cols(m, sa[0], sa[1], spot)
                                        and got.total_weight.hex() == m.total_weight.hex())
             r["ms_reference"] = 1e3 * _time(lambda: spot.mapping.map_devices(
                 *sa[:4], inheritance=sa[4], requests_by_old_pipeline=sa[5], fused_weight=sa[6]), ref_reps)
