@@ -251,10 +251,23 @@ typedef struct sk_exec_chunk {
 } sk_exec_chunk; /* 32 bytes */
 
 int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages);
+/* Zero a control block (flags down) ahead of a run, e.g. before handing its
+ * IPC handle to a consumer that will wait on the stage flags. */
+int sk_exec_reset(uint32_t* d_ctl, int n_rounds, int n_stages, void* stream);
 int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_round_total, int n_rounds,
                  const int32_t* d_stage_round, int n_stages, uint32_t* d_ctl,
                  const uint32_t* const* d_peer_progress, int n_peers, int n_ctas, double timeout_s,
                  void* stream);
+
+/* Consumer side of the stage-ready flags (e.g. a serving process that maps
+ * a context daemon's control block with CUDA IPC): work queued on `stream`
+ * after this call runs only once *d_flag >= value.  d_status (optional)
+ * receives 0, or 1 if timeout_s passed first. */
+int sk_wait_flag(const uint32_t* d_flag, uint32_t value, double timeout_s, uint32_t* d_status, void* stream);
+/* The same wait as a stream memory operation (cuStreamWaitValue32, GEQ):
+ * executed by the stream's front end, no SM held -- use it when the flag's
+ * producer is a kernel of another process on the same GPU. */
+int sk_stream_wait_flag(const uint32_t* d_flag, uint32_t value, void* stream);
 
 /* Copy-engine comparison path: one cudaMemcpyAsync per (HOST array) entry,
  * in order, on `stream`.  sk_d2h: blocking device -> host copy (control
@@ -340,6 +353,11 @@ typedef struct sk_mig_result sk_mig_result; /* opaque, library-owned */
  * SK_ENOSOURCE: sk_planner_error() holds "<lo> <hi>" numerators of the
  * uncovered piece. */
 int sk_plan_migration(const sk_mig_input* in, int derive_only, sk_mig_result** out);
+/* Many independent plans on a pool of n_threads host threads (0 = all
+ * cores): per plan status[i], outs[i] (free each with sk_mig_free), and for
+ * SK_ENOSOURCE the uncovered piece's numerators in err_range[2i..2i+1]. */
+int sk_plan_migration_many(const sk_mig_input* ins, int n, int derive_only, int n_threads,
+                           sk_mig_result** outs, int32_t* status, int64_t* err_range);
 /* counts[7] = {transfers, actions, action_transfers, releases, peak entries,
  *              layer_releases, model transfers} */
 int sk_mig_counts(const sk_mig_result* r, int64_t* counts);
@@ -401,6 +419,33 @@ int sk_migration_cost_batched(const sk_tl_plan* d_plans, int n_plans, const int3
                               const uint8_t* d_has_release, const double* d_release,
                               double* d_scratch, uint8_t* d_flags, double bandwidth,
                               double latency, double* d_cost, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Candidate scoring (estimator.cu): exec_latency / throughput
+ * (costmodel.py:121-183) for many (config, workload) queries and the
+ * controller's choice optimize_config (controller.py:79-117) for many
+ * (n_available, obtainable, rate) scenarios, on the device, bit-identical.
+ * Profile tables: per profiled (P,M,B) shape s: decode[s] seconds; prefill
+ * points pre_s/pre_v[pre_ptr[s] .. pre_ptr[s+1]) with s_in ascending.
+ */
+typedef struct sk_est_query {
+  int32_t shape;  /* profiled (P,M,B) shape index */
+  int32_t D, P, B;
+  int64_t s_in, s_out;
+} sk_est_query; /* 32 bytes */
+
+/* d_latency[i] = exec_latency(query i); d_phi (optional) = D*B / (latency /
+ * (P * eta)) -- throughput() when s_in/s_out are the profile's nominal ones. */
+int sk_score_configs(const sk_est_query* d_q, int n, const double* d_decode, const int32_t* d_pre_ptr,
+                     const int64_t* d_pre_s, const double* d_pre_v, double eta, double* d_latency,
+                     double* d_phi, void* stream);
+/* Candidates in ascending (D,P,M,B) order with instance count, nominal phi
+ * and latency; per scenario the chosen candidate index, or -1 (nothing fits).
+ * band = 1 + LATENCY_SIMILARITY as the reference computes it. */
+int sk_select_configs(const int32_t* d_n_inst, const double* d_phi, const double* d_latency, int n_cfg,
+                      const int32_t* d_n_available, const int32_t* d_obtainable, const double* d_rate,
+                      int n_queries, double band, int32_t* d_choice, void* stream);
+const char* sk_estimator_error(void);
 
 /* memopt_layer_order (migration.py:114-143) on per-layer traffic given as CSR
  * lists of (instance, bytes): incoming[l] and freed[l] for l in 0..L-1.

@@ -37,7 +37,13 @@ from .planner import (  # noqa: F401
     migration_cost,
     plan_from_dict,
     plan_migration,
+    plan_migration_many,
     plan_timeline,
     plan_to_dict,
     simulate_buffer_usage,
+)
+from .estimator import (  # noqa: F401
+    exec_latency_many,
+    optimize_config_many,
+    throughput_many,
 )

@@ -16,7 +16,8 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SRC = [PKG / "csrc" / "spotkm.cu", PKG / "csrc" / "planner.cpp", PKG / "csrc" / "reshard.cu"]
+SRC = [PKG / "csrc" / "spotkm.cu", PKG / "csrc" / "planner.cpp", PKG / "csrc" / "reshard.cu",
+       PKG / "csrc" / "estimator.cu"]
 OUT = PKG / "_lib" / "libspotkm.so"
 
 NVCC_FLAGS = [
@@ -53,7 +54,7 @@ def build_hostpack(force: bool = False) -> Path:
 def build(force: bool = False, verbose: bool = False) -> Path:
     build_hostpack(force)
     OUT.parent.mkdir(parents=True, exist_ok=True)
-    newest = max(p.stat().st_mtime for p in SRC + [ROOT / "include" / "spotkm.h"])
+    newest = max(p.stat().st_mtime for p in SRC + [ROOT / "include" / "spotkm.h", PKG / "csrc" / "exact.cuh"])
     if not force and OUT.exists() and OUT.stat().st_mtime >= newest:
         return OUT
     cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", str(OUT),

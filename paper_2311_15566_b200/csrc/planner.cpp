@@ -22,6 +22,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <map>
 #include <string>
@@ -589,6 +591,36 @@ int sk_plan_migration(const sk_mig_input* in, int derive_only, sk_mig_result** o
   }
   R->peak = plan.peak;
   *out = R;
+  return SK_OK;
+}
+
+// Many independent plans at once ("host, one thread per
+// plan"): a pool of n_threads std::threads takes plans in index order.  Per
+// plan: status[i] (sk_status), outs[i] (NULL unless SK_OK), and for
+// SK_ENOSOURCE the uncovered piece's numerators in err_range[2i..2i+1].
+int sk_plan_migration_many(const sk_mig_input* ins, int n, int derive_only, int n_threads,
+                           sk_mig_result** outs, int32_t* status, int64_t* err_range) {
+  if (n <= 0) return SK_OK;
+  if (n_threads <= 0) n_threads = (int)std::thread::hardware_concurrency();
+  if (n_threads <= 0) n_threads = 1;
+  if (n_threads > n) n_threads = n;
+  std::atomic<int> next(0);
+  auto work = [&]() {
+    for (int i = next++; i < n; i = next++) {
+      outs[i] = nullptr;
+      status[i] = sk_plan_migration(&ins[i], derive_only, &outs[i]);
+      if (status[i] == SK_ENOSOURCE && err_range) {
+        long long lo = 0, hi = 0;
+        sscanf(g_perr, "%lld %lld", &lo, &hi);
+        err_range[2 * i] = lo;
+        err_range[2 * i + 1] = hi;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < n_threads; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
   return SK_OK;
 }
 

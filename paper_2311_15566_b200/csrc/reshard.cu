@@ -13,6 +13,7 @@
 // compared byte for byte (SURVEY.md 8(d) "reshared tensors byte-identical").
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -93,6 +94,26 @@ __global__ void __launch_bounds__(kR_TPB) k_verify(const sk_region* __restrict__
 //   then n_stages stage flags, then (8-B aligned) n_stages + 1 u64 stamps:
 //   the launch start and each stage's ready time (ns, %globaltimer).
 
+// a consumer-side wait on a (possibly IPC-mapped) device flag: one thread
+// spins until *flag >= value, so work queued after it on the stream runs only
+// once the producer has raised the flag; status = 0 ok, 1 timeout
+__global__ void k_wait_flag(const unsigned* flag, unsigned value, unsigned long long timeout_ns,
+                            unsigned* status) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*reinterpret_cast<const volatile unsigned*>(flag) < value) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) {
+      if (status) *status = 1u;
+      return;
+    }
+    __nanosleep(1000);
+  }
+  __threadfence_system();
+  if (status) *status = 0u;
+}
+
 constexpr int kX_TPB = 512;
 
 __device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
@@ -136,6 +157,7 @@ __device__ unsigned global_progress(const ExecArgs& A) {
 __global__ void __launch_bounds__(kX_TPB) k_exec(const ExecArgs A) {
   __shared__ int s_idx;
   __shared__ int s_abort;
+  __shared__ unsigned s_g;  // global progress last seen by this CTA (block-uniform)
   const unsigned long long t0 = global_ns();
   if (blockIdx.x == 0) {
     // ---- monitor ----
@@ -175,7 +197,7 @@ __global__ void __launch_bounds__(kX_TPB) k_exec(const ExecArgs A) {
     return;
   }
   // ---- workers ----
-  unsigned cached_g = 0;
+  if (threadIdx.x == 0) s_g = 0;
   while (true) {
     if (threadIdx.x == 0) {
       s_idx = (int)atomicAdd(A.ctl + 0, 1u);
@@ -185,12 +207,15 @@ __global__ void __launch_bounds__(kX_TPB) k_exec(const ExecArgs A) {
     const int idx = s_idx;
     if (idx >= A.n_chunks) break;
     const sk_exec_chunk c = A.chunks[idx];
-    if (c.wait_round >= 0 && cached_g <= (unsigned)c.wait_round) {
+    // (s_g is read by every thread after the barrier above and written only
+    // by thread 0 between two barriers: the branch is block-uniform)
+    if (c.wait_round >= 0 && s_g <= (unsigned)c.wait_round) {
       if (threadIdx.x == 0) {
         // recycled space: every rank must be past round wait_round
         while (true) {
-          cached_g = global_progress(A);
-          if (cached_g > (unsigned)c.wait_round) break;
+          const unsigned g = global_progress(A);
+          s_g = g;
+          if (g > (unsigned)c.wait_round) break;
           if (ld_volatile_u32(A.ctl + 2) != 0u || global_ns() - t0 > A.timeout_ns) {
             atomicCAS(A.ctl + 2, 0u, 1u);  // worker timeout
             s_abort = 1;
@@ -296,6 +321,47 @@ int sk_memcpy_batched(const sk_copy* h_copies, int n, void* stream) {
 int sk_d2h(void* h_dst, const void* d_src, uint64_t bytes) {
   cudaError_t e = cudaMemcpy(h_dst, d_src, bytes, cudaMemcpyDeviceToHost);
   return e == cudaSuccess ? SK_OK : rfail("cudaMemcpy D2H", e);
+}
+
+int sk_wait_flag(const uint32_t* d_flag, uint32_t value, double timeout_s, uint32_t* d_status, void* stream) {
+  k_wait_flag<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_flag, value,
+                                                                (unsigned long long)(timeout_s * 1e9), d_status);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SK_OK : rfail("k_wait_flag launch", e);
+}
+
+// cuStreamWaitValue32 from the driver, resolved at run time (no link-time
+// libcuda dependency): a wait executed by the stream's front end, not by a
+// kernel, so it holds no SM -- the right primitive when the producer is a
+// kernel of ANOTHER process on the same GPU (contexts time-slice; a spinning
+// consumer kernel can starve the producer).
+typedef int (*wait_value_fn)(void* stream, unsigned long long addr, uint32_t value, unsigned flags);
+
+int sk_stream_wait_flag(const uint32_t* d_flag, uint32_t value, void* stream) {
+  static wait_value_fn fn = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return (wait_value_fn) nullptr;
+    void* f = dlsym(h, "cuStreamWaitValue32_v2");
+    if (!f) f = dlsym(h, "cuStreamWaitValue32");
+    return reinterpret_cast<wait_value_fn>(f);
+  }();
+  if (!fn) {
+    snprintf(g_rerr, sizeof g_rerr, "cuStreamWaitValue32 not available");
+    return SK_ECUDA;
+  }
+  const int rc = fn(stream, (unsigned long long)(uintptr_t)d_flag, value, 0x0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+  if (rc != 0) {
+    snprintf(g_rerr, sizeof g_rerr, "cuStreamWaitValue32 failed: CUresult %d", rc);
+    return SK_ECUDA;
+  }
+  return SK_OK;
+}
+
+int sk_exec_reset(uint32_t* d_ctl, int n_rounds, int n_stages, void* stream) {
+  const int64_t w = 4 + (int64_t)n_rounds + n_stages;
+  const size_t bytes = (size_t)(((w + 1) & ~(int64_t)1) * 4 + 8 * (int64_t)(n_stages + 1));
+  cudaError_t e = cudaMemsetAsync(d_ctl, 0, bytes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? SK_OK : rfail("exec control reset", e);
 }
 
 int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages) {

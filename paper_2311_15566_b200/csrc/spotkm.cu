@@ -265,41 +265,69 @@ __host__ __device__ __forceinline__ void hungarian_small(const double (&w)[N][N]
 // ---------------------------------------------------------------------------
 // K1: dense weights, two adjacent columns per thread (16-B stores)
 
-constexpr int kW_TPB = 128;
+constexpr int kW_TPB = 256;
+constexpr int kW_MAXC = 2048;  // plans up to this many columns decode them once into shared memory
+constexpr int kW_RPB = 16;     // rows per block: the column table is built once per 16 rows
 
+// One block per (plan, 16 rows).  The plan's column decode (stage layer block,
+// shard interval, pipeline; domain.py:92-99, 271-288) is built once into a
+// shared table, so each entry is two segment overlaps, one int -> double
+// conversion and one exact scaling -- and the row is written with coalesced
+// 16-byte stores (two adjacent columns per thread).
 __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ plans,
                                                     const int32_t* __restrict__ row_ptr,
                                                     const sk_segment* __restrict__ segs,
                                                     double* __restrict__ W) {
-  const sk_plan p = plans[blockIdx.z];
-  const int r = blockIdx.y;
-  if (r >= p.rows) return;
+  __shared__ int4 ctab[kW_MAXC];
+  const sk_plan p = plans[blockIdx.y];
+  const int r0 = blockIdx.x * kW_RPB;
+  if (r0 >= p.rows) return;
+  const int r1 = min(p.rows, r0 + kW_RPB);
   const int C = p.D * p.P * p.M;
-  const int c = 2 * (blockIdx.x * kW_TPB + threadIdx.x);
-  if (c >= C) return;
-  if (p.flags & SK_PLAN_GENERIC) {  // block-uniform
-    double* o = W + p.f_off + (long long)r * C + c;
-    o[0] = weight_generic(p, row_ptr, segs, r, c);
-    if (c + 1 < C) o[1] = weight_generic(p, row_ptr, segs, r, c + 1);
+  if ((p.flags & SK_PLAN_GENERIC) || C > kW_MAXC || p.L > 0xffff) {  // block-uniform
+    const bool gen = (p.flags & SK_PLAN_GENERIC) != 0;
+    for (long long e = threadIdx.x; e < (long long)(r1 - r0) * C; e += kW_TPB) {
+      const int r = r0 + (int)(e / C), c = (int)(e % C);
+      W[p.f_off + (long long)r * C + c] = gen ? weight_generic(p, row_ptr, segs, r, c)
+                                              : weight_at(p, row_ptr, segs, r, c);
+    }
     return;
   }
-  const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
-  const Col ca = col_of(p, c);
-  const bool two = c + 1 < C;
-  const Col cb = two ? col_of(p, c + 1) : ca;
-  long long na = 0, nb = 0;
-  for (int s = s0; s < s1; ++s) {
-    const sk_segment sg = segs[s];
-    na += seg_num(sg, ca);
-    nb += seg_num(sg, cb);
+  for (int c = threadIdx.x; c < C; c += kW_TPB) {
+    const Col x = col_of(p, c);
+    ctab[c] = make_int4(x.s0 | (x.s1 << 16), x.i0, x.i1, x.d);
   }
-  double* out = W + p.f_off + (long long)r * C + c;
-  const double wa = num_to_w(na, p.K), wb = num_to_w(nb, p.K);
-  if (two && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-    *reinterpret_cast<double2*>(out) = make_double2(wa, wb);
-  } else {
-    out[0] = wa;
-    if (two) out[1] = wb;
+  __syncthreads();
+  // N / K: the exact reciprocal product when K is a power of two (bit-identical
+  // to the correctly rounded division), else the IEEE division
+  const bool pow2 = (p.K & (p.K - 1)) == 0;
+  const double inv = 1.0 / (double)p.K;
+  for (int r = r0; r < r1; ++r) {
+    const int sb = row_ptr[p.row_base + r], se = row_ptr[p.row_base + r + 1];
+    double* out = W + p.f_off + (long long)r * C;
+    const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    for (int c = 2 * threadIdx.x; c < C; c += 2 * kW_TPB) {
+      const bool two = c + 1 < C;
+      const int4 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
+      long long na = 0, nb = 0;
+      for (int k = sb; k < se; ++k) {
+        const sk_segment sg = segs[k];
+        const int la0 = max(sg.l0, ta.x & 0xffff), la1 = min(sg.l1, (int)((unsigned)ta.x >> 16));
+        const int lb0 = max(sg.l0, tb.x & 0xffff), lb1 = min(sg.l1, (int)((unsigned)tb.x >> 16));
+        const int ia = min(sg.b, ta.z) - max(sg.a, ta.y), ib = min(sg.b, tb.z) - max(sg.a, tb.y);
+        const bool pa = sg.pipe == 0 || sg.pipe == ta.w, pb = sg.pipe == 0 || sg.pipe == tb.w;
+        if (la1 > la0 && ia > 0 && pa) na += (long long)(la1 - la0) * ia * sg.unit;
+        if (lb1 > lb0 && ib > 0 && pb) nb += (long long)(lb1 - lb0) * ib * sg.unit;
+      }
+      const double wa = pow2 ? __ll2double_rn(na) * inv : num_to_w(na, p.K);
+      const double wb = pow2 ? __ll2double_rn(nb) * inv : num_to_w(nb, p.K);
+      if (two && vec) {
+        *reinterpret_cast<double2*>(out + c) = make_double2(wa, wb);
+      } else {
+        out[c] = wa;
+        if (two) out[c + 1] = wb;
+      }
+    }
   }
 }
 
@@ -1668,11 +1696,10 @@ int sk_build_weights(const sk_plan* d_plans, int n_plans, const int32_t* d_row_p
                      const sk_segment* d_segs, double* d_W, int max_rows, int max_cols, void* stream) {
   if (n_plans < 0 || max_rows < 0 || max_cols < 0) return set_err(SK_EINVAL, "negative sizes");
   if (n_plans == 0 || max_rows == 0 || max_cols == 0) return SK_OK;
-  if (max_rows > kMaxGridY) return set_err(SK_EINVAL, "rows %d > %d", max_rows, kMaxGridY);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
     const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
-    dim3 grid((max_cols + 2 * kW_TPB - 1) / (2 * kW_TPB), max_rows, np);
+    dim3 grid((max_rows + kW_RPB - 1) / kW_RPB, np);
     k_weights<<<grid, kW_TPB, 0, s>>>(d_plans + p0, d_row_ptr, d_segs, d_W);
     int rc = cuda_check("k_weights launch");
     if (rc) return rc;

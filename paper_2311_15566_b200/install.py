@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import sys
 
+from . import estimator as _estimator
 from . import mapping as _mapping
 from . import planner as _planner
 
@@ -29,6 +30,10 @@ PARTS = {
                 "simulate_buffer_usage": _planner.simulate_buffer_usage},
     "estimator": {"plan_timeline": _planner.plan_timeline,
                   "migration_cost": _planner.migration_cost},
+    # opt-in: device-batched candidate scoring; per single call it pays a
+    # device round trip, so the default install leaves the reference's here
+    "controller": {"exec_latency": _estimator.exec_latency, "throughput": _estimator.throughput,
+                   "optimize_config": _estimator.optimize_config},
 }
 
 _saved: list = []

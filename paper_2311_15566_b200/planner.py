@@ -84,6 +84,8 @@ def _lib():
         lib.sk_migration_cost.restype = i32
         lib.sk_simulate_buffer_usage.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.sk_simulate_buffer_usage.restype = i32
+        lib.sk_plan_migration_many.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+        lib.sk_plan_migration_many.restype = i32
         lib.sk_rat_to_double.argtypes = [i64, ctypes.c_uint64, i64]
         lib.sk_rat_to_double.restype = dbl
         lib._planner_sigs = True
@@ -181,18 +183,20 @@ class _Flat:
         return s
 
 
-def _run(flat, u_max, derive_only, T):
+def _raise(flat, rc, T, lo=None, hi=None):
     lib = _lib()
-    s = flat.struct(u_max)
-    res = ctypes.c_void_p()
-    rc = lib.sk_plan_migration(ctypes.byref(s), 1 if derive_only else 0, ctypes.byref(res))
     if rc == nat.SK_ENOSOURCE:
-        lo, hi = (int(x) for x in lib.sk_planner_error().decode().split())
+        if lo is None:
+            lo, hi = (int(x) for x in lib.sk_planner_error().decode().split())
         raise T.MigrationError(
             f"no source holds required shard [{Fraction(lo, flat.K)},{Fraction(hi, flat.K)}): "
             "layout inconsistent with mapping")
-    if rc != nat.SK_OK:
-        raise T.MigrationError(lib.sk_planner_error().decode())
+    raise T.MigrationError(lib.sk_planner_error().decode())
+
+
+def _export(res):
+    """Copy a native sk_mig_result into numpy arrays, then free it."""
+    lib = _lib()
     try:
         counts = np.zeros(7, dtype=np.int64)
         lib.sk_mig_counts(res, _p(counts))
@@ -206,6 +210,16 @@ def _run(flat, u_max, derive_only, T):
     finally:
         lib.sk_mig_free(res)
     return counts, tr, ac, at, rl, pk, lr
+
+
+def _run(flat, u_max, derive_only, T):
+    lib = _lib()
+    s = flat.struct(u_max)
+    res = ctypes.c_void_p()
+    rc = lib.sk_plan_migration(ctypes.byref(s), 1 if derive_only else 0, ctypes.byref(res))
+    if rc != nat.SK_OK:
+        _raise(flat, rc, T)
+    return _export(res)
 
 
 def _transfers(flat, tr, n, T):
@@ -256,7 +270,11 @@ def plan_migration(mapping, old_layout, model, u_max=None, inherited_by_pipeline
     if mapping.config is None:
         raise T.MigrationError("mapping carries no target config")
     flat = _Flat(mapping, old_layout, model, inherited_by_pipeline, departing)
-    counts, tr, ac, at, rl, pk, _ = _run(flat, u_max, False, T)
+    return _build_plan(flat, _run(flat, u_max, False, T), u_max, T)
+
+
+def _build_plan(flat, exported, u_max, T):
+    counts, tr, ac, at, rl, pk, _ = exported
     allt = _transfers(flat, tr, int(counts[0]), T)
     at = at[:int(counts[2])].tolist()
     rel = [(flat.insts[i], b) for i, _, b in rl[:int(counts[3])].tolist()]
@@ -269,6 +287,54 @@ def plan_migration(mapping, old_layout, model, u_max=None, inherited_by_pipeline
     plan = T.MigrationPlan(actions=actions, u_max=u_max)
     plan.peak_usage = {name: float(pk[i]) for i, name in enumerate(flat.insts)}
     return plan
+
+
+def plan_migration_many(problems, threads: int = 0) -> list:
+    """`plan_migration` for many independent problems (host,
+    one thread per plan): each problem is the argument tuple
+    (mapping, old_layout, model[, u_max[, inherited_by_pipeline[, departing]]]).
+    The caller's objects are flattened here; the planning itself runs in ONE
+    native call on a pool of `threads` host threads (0 = all cores, GIL
+    released).  Returns one MigrationPlan per problem, or the exception the
+    single call would raise, in place (not raised)."""
+    flats, structs, Ts, umax = [], [], [], []
+    for args in problems:
+        mapping, old_layout, model = args[:3]
+        u_max = args[3] if len(args) > 3 else None
+        inh = args[4] if len(args) > 4 else None
+        dep = args[5] if len(args) > 5 else frozenset()
+        T = result_types(mapping)
+        if mapping.config is None:
+            flats.append(T.MigrationError("mapping carries no target config"))
+            structs.append(None)
+        else:
+            f = _Flat(mapping, old_layout, model, inh, dep)
+            flats.append(f)
+            structs.append(f.struct(u_max))
+        Ts.append(T)
+        umax.append(u_max)
+    idx = [i for i, st in enumerate(structs) if st is not None]
+    n = len(idx)
+    arr = (_MigInput * max(n, 1))(*[structs[i] for i in idx])
+    outs = (ctypes.c_void_p * max(n, 1))()
+    status = np.zeros(max(n, 1), dtype=np.int32)
+    err = np.zeros(2 * max(n, 1), dtype=np.int64)
+    if n:
+        _lib().sk_plan_migration_many(ctypes.cast(arr, ctypes.c_void_p), n, 0, int(threads),
+                                      ctypes.cast(outs, ctypes.c_void_p), _p(status), _p(err))
+    results = list(flats)
+    for k, i in enumerate(idx):
+        f, T = flats[i], Ts[i]
+        if status[k] != nat.SK_OK:
+            if outs[k]:
+                _lib().sk_mig_free(outs[k])
+            try:
+                _raise(f, int(status[k]), T, int(err[2 * k]), int(err[2 * k + 1]))
+            except Exception as e:  # noqa: BLE001
+                results[i] = e
+            continue
+        results[i] = _build_plan(f, _export(outs[k]), umax[i], T)
+    return results
 
 
 def memopt_layer_order(traffic_by_layer, u_max):

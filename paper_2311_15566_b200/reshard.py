@@ -408,6 +408,8 @@ def _exec_lib():
         lib.sk_exec_plan.restype = i32
         lib.sk_memcpy_batched.argtypes = [vp, i32, vp]
         lib.sk_memcpy_batched.restype = i32
+        lib.sk_exec_reset.argtypes = [vp, i32, i32, vp]
+        lib.sk_exec_reset.restype = i32
         lib.sk_d2h.argtypes = [vp, vp, ctypes.c_uint64]
         lib.sk_d2h.restype = i32
         lib._exec_sigs = True
@@ -586,11 +588,16 @@ class ReshardExecutor:
         for i, (s, d, n, _, _) in enumerate(self.transfers_issued):
             tr[i] = (s, d, n)
         self.h_transfers = tr
-        self.d_fill = self._regions(seed, new=False)
-        self.d_check = self._regions(seed, new=True)
+        self.seed = seed
+        self.d_fill = self._regions(new=False)
+        self.d_check = self._regions(new=True)
         self.d_bad = torch.zeros(1, dtype=torch.int64, device=dev)
 
-    def _regions(self, seed, new: bool):
+    def region_rows(self, new: bool, seed: int | None = None):
+        """[(gpu ref, (ptr, bytes, pattern key, object byte base))] of this
+        rank's old contexts (new=False) or new contexts (every kept and
+        received piece, new=True)."""
+        seed = self.seed if seed is None else seed
         rids = sorted({k[1] for gl in self.layout.gpus.values() for r in gl.old for k in [r.key] if k[0] == "c"}
                       | {p[0][1] for gl in self.layout.gpus.values() for p in gl.pieces if p[0][0] == "c"})
         rid_index = {r: i for i, r in enumerate(rids)}
@@ -605,11 +612,15 @@ class ReshardExecutor:
                 continue
             if new:
                 for key, lo, hi, tok, unit, off in gl.pieces:
-                    rows.append((self.base[g] + off, _span(hi - lo, unit), key_of(key), _span(lo, unit)))
+                    rows.append((g, (self.base[g] + off, _span(hi - lo, unit), key_of(key), _span(lo, unit))))
             else:
                 for reg in gl.old:
-                    rows.append((self.base[g] + reg.off, _span(reg.hi - reg.lo, reg.unit), key_of(reg.key),
-                                 _span(reg.lo, reg.unit)))
+                    rows.append((g, (self.base[g] + reg.off, _span(reg.hi - reg.lo, reg.unit), key_of(reg.key),
+                                     _span(reg.lo, reg.unit))))
+        return rows
+
+    def _regions(self, new: bool):
+        rows = [r for _, r in self.region_rows(new)]
         reg = np.zeros(len(rows), dtype=nat.REGION)
         for i, r in enumerate(rows):
             reg[i] = r
@@ -633,6 +644,11 @@ class ReshardExecutor:
             self.d_totals.data_ptr() if self.d_totals is not None else 0, self.n_rounds,
             self.d_stages.data_ptr() if self.d_stages is not None else 0, len(self.stages),
             self.slab.ptr, self.d_peers.data_ptr(), self.n_peers, n_ctas, self.timeout_s, st))
+
+    def reset_control(self):
+        """Zero the control block (every stage flag down) on the current stream."""
+        nat.check(self.lib.sk_exec_reset(self.slab.ptr, self.n_rounds, len(self.stages),
+                                         torch.cuda.current_stream().cuda_stream))
 
     def run_unordered(self, n_ctas: int = 0):
         """Data path only: the same chunks in one k_copy launch with no round
@@ -725,13 +741,13 @@ U_MAX = 4e9   # the B_S scenario's migration buffer cap (data/scenario_bs.json:1
 
 
 def make_reshard_problem(geom, old_shape, new_shape, batch: int = 8, seq: int = 2048,
-                         u_max: float | None = U_MAX, mapper=None):
+                         u_max: float | None = U_MAX, mapper=None, with_mapping: bool = False):
     """One GPU per instance (G=1), old config laid out positionally on i-0..i-(N-1),
     `batch` cached requests of `seq` tokens per old pipeline, identity
     inheritance.  The mapping and plan come from this package's device mapper
     (or `mapper`, same signature) and native planner (memory-optimised layer
     order under `u_max`).
-    Returns (plan, old_layout, new_required, model, refs)."""
+    Returns (plan, old_layout, new_required, model, refs[, mapping])."""
     from . import domain as dm
     from .mapping import default_inheritance, map_devices
     from .planner import plan_migration
@@ -764,4 +780,7 @@ def make_reshard_problem(geom, old_shape, new_shape, batch: int = 8, seq: int = 
     need = required_layout(mapping, model, inherited, dm.ContextInventory)
     for ref in layout:
         need.setdefault(ref, dm.ContextInventory())
-    return plan, layout, need, model, [(f"i-{k}", 0) for k in range(n)]
+    refs = [(f"i-{k}", 0) for k in range(n)]
+    if with_mapping:
+        return plan, layout, need, model, refs, mapping
+    return plan, layout, need, model, refs

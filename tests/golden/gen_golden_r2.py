@@ -318,11 +318,53 @@ def gen_models_bs():
     return maps, plans
 
 
+# ---------------------------------------------------------------------------
+# 4. candidate scoring: exec_latency / throughput / optimize_config
+
+def gen_estimator():
+    from spotsim import controller as ref_ctl
+    from spotsim import costmodel as ref_cost
+
+    out = {}
+    for prof in ("gpt-20b", "opt-6.7b", "llama-30b"):
+        profile = ref_cost.load_profile(bundled_path(prof))
+        cands = ref_ctl.candidate_configs(profile, max_gpus=64)
+        lat = []
+        for cfg in cands:
+            for s_in, s_out in ((512, 128), (128, 0), (1000, 64), (2048, 512), (1, 1), (700, 3), (96, 7),
+                                (4096, 1)):
+                try:
+                    v = ref_cost.exec_latency(profile, cfg, s_in, s_out)
+                    lat.append([list(cfg.as_tuple()), s_in, s_out, hx(v)])
+                except ref_cost.ProfileMissError:
+                    lat.append([list(cfg.as_tuple()), s_in, s_out, None])
+        phi = [[list(c.as_tuple()), hx(ref_cost.throughput(profile, c))] for c in cands]
+        dec = []
+        for G in (1, 4):
+            for n_av in range(0, 22):
+                for rate in (0.0, 0.1, 0.25, 0.35, 0.55, 1.0, 2.0, 3.5, 5.0, 10.0, 40.0):
+                    for lim in (None, n_av + 2, max(n_av - 1, 0)):
+                        c = ref_ctl.optimize_config(n_av, None, rate, profile, cands, gpus_per_instance=G,
+                                                    cloud_limit=lim)
+                        dec.append([G, n_av, rate, lim, None if c is None else list(c.as_tuple())])
+        tables = {"decode": [[*k, hx(v)] for k, v in sorted(profile.decode_table.items())],
+                  "prefill": [[*k, s_, hx(v)] for k, d in sorted(profile.prefill_table.items())
+                              for s_, v in sorted(d.items())],
+                  "eta": hx(profile.pipeline_efficiency),
+                  "nominal": [profile.nominal_s_in, profile.nominal_s_out]}
+        out[prof] = {"latency": lat, "throughput": phi, "decisions": dec, "profile": tables}
+    return out
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "estimator":
+        save("estimator", {"meta": META, "profiles": gen_estimator()})
+        return
     rng = np.random.default_rng(20261019)
     edge = gen_edge(rng)
     kmw = gen_km_wide(rng)
     save("edge", {"meta": META, "cases": edge, "km": kmw})
+    save("estimator", {"meta": META, "profiles": gen_estimator()})
     maps, plans = gen_models_bs()
     save("models_bs", {"meta": META, "maps": maps, "plans": plans})
     t0 = time.perf_counter()

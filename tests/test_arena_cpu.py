@@ -121,3 +121,19 @@ def test_memopt_order_changes_the_arena_peak():
         peaks[u] = max(d["arena_bytes"] - d["old_bytes"] for d in rep.values())
         assert abs(peaks[u] - max(plan.peak_usage.values())) <= 0.001 * peaks[u] + 4096 * ALIGN
     assert peaks[4e9] <= peaks[None]
+
+
+def test_daemon_wire_format_roundtrip():
+    """The context daemon's request (plan_to_dict + layouts + mapping, JSON)
+    decodes to the same plan and inventories (paper_2311_15566_b200/daemon.py)."""
+    import json
+
+    from paper_2311_15566_b200 import daemon, planner
+
+    plan, layout, need, model, refs, mapping = reshard.make_reshard_problem(
+        SMALL, (1, 2, 2), (1, 1, 4), 3, 64, mapper=port_mapper, with_mapping=True)
+    req = json.loads(json.dumps(daemon.migrate_request(plan, layout, need, model, mapping.assignment)))
+    assert planner.plan_to_dict(planner.plan_from_dict(req["plan"])) == planner.plan_to_dict(plan)
+    assert {(i, g): daemon.dec_inv(v) for i, g, v in req["old"]} == layout
+    assert {(i, g): daemon.dec_inv(v) for i, g, v in req["new"]} == need
+    assert len(req["assignment"]) == len(mapping.assignment)

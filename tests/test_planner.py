@@ -163,3 +163,23 @@ def test_rat_to_double_correctly_rounded():
         den = rng.randrange(1, 1 << rng.choice([3, 20, 31, 40]))
         got = lib.sk_rat_to_double(num >> 64, num & ((1 << 64) - 1), den)
         assert got == float(Fraction(num, den)), (num, den)
+
+
+def test_plan_migration_many_equals_single_calls(golden):
+    """The threaded batch (one native call, a pool of host threads) returns
+    exactly the single-call plans, errors in place."""
+    docs = golden("plans")["cases"] + golden("scenario")["plans"]
+    probs = []
+    for doc in docs:
+        model, mapping, layout, inh, dep = rebuild(doc)
+        probs.append((mapping, layout, model, doc["u_max"], inh, dep))
+    for threads in (1, 4, 0):
+        got = planner.plan_migration_many(probs, threads=threads)
+        assert len(got) == len(docs)
+        for g, doc in zip(got, docs):
+            if doc["error"]:
+                assert isinstance(g, sk.MigrationError)
+                if "message" in doc:
+                    assert str(g) == doc["message"]
+            else:
+                assert planner.plan_to_dict(g) == doc["plan"]

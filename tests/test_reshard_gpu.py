@@ -12,7 +12,7 @@ import torch
 
 from paper_2311_15566_b200 import planner, reshard
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(300)]
 
 SMALL = ("toy-bf16", 8, 8 * 1024 * 64, 1024)
 TRANSITIONS = [((1, 2, 2), (1, 1, 4)), ((1, 2, 4), (2, 1, 4)), ((1, 4, 2), (1, 2, 4)),
@@ -103,6 +103,7 @@ def test_executor_ingests_the_json_wire_plan():
 
 
 @pytest.mark.parametrize("geom,old,new", [(reshard.GPT20B_BF16, (1, 4, 2), (1, 2, 4))])
+@pytest.mark.timeout(600)
 def test_full_geometry_emulated(geom, old, new):
     """BASELINE.json configs[3] at its real size -- GPT-20B bf16 (1,4,2)->(1,2,4),
     KV batch 8 x seq 2048, 8 GPU refs emulated on this device (~75 GB of

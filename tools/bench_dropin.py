@@ -41,7 +41,9 @@ def load_spotsim():
                 sys.path.append(str(cand))
             try:
                 import spotsim
+                import spotsim.controller  # noqa: F401
                 import spotsim.costmodel  # noqa: F401
+                import spotsim.data  # noqa: F401
                 import spotsim.domain  # noqa: F401
                 import spotsim.mapping  # noqa: F401
                 import spotsim.migration  # noqa: F401
@@ -311,6 +313,81 @@ def dropin_block(spot, ref_reps: int = 1):
                 smap, slay, sm, u_max=d["u_max"], inherited_by_pipeline=sinh, departing=sdep), ref_reps)
         prow.append(r)
     out["plan_migration"] = _summary(prow)
+    # plan_migration_many: the scenario's plans x 8 on all host threads, vs
+    # the same plans one call at a time
+    probs = []
+    for d in doc["plans"]:
+        if not d["error"]:
+            model, mapping, layout, inh_, dep = rebuild(d)
+            probs.append((mapping, layout, model, d["u_max"], inh_, dep))
+    batch = probs * 8
+    t_many = _time(lambda: planner.plan_migration_many(batch, threads=0), 2)
+    t_one = _time(lambda: [planner.plan_migration(*p[:3], u_max=p[3], inherited_by_pipeline=p[4],
+                                                  departing=p[5]) for p in batch], 1)
+    out["plan_migration_many"] = {"plans": len(batch), "threads": os.cpu_count(), "ms": 1e3 * t_many,
+                                  "ms_sequential": 1e3 * t_one, "speedup_vs_sequential": t_one / t_many}
+    out["optimize_config_many"] = _guarded(lambda: controller_leg(spot))
+    return out
+
+
+def _guarded(fn):
+    try:
+        return fn()
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
+def controller_leg(spot, n_scen: int = 20000):
+    """optimize_config (controller.py:79-117) for many (n_available, rate,
+    cloud_limit) scenarios: one device batch vs the reference one call at a
+    time (a timed sample), on the GPT-20B profile's candidates up to 64 GPUs;
+    the sampled reference decisions are checked against the batch's."""
+    import random
+    from types import SimpleNamespace
+
+    import torch
+
+    from fmt import load, unhx
+
+    import paper_2311_15566_b200 as sk
+    from paper_2311_15566_b200 import estimator
+
+    t = load("estimator")["profiles"]["gpt-20b"]
+    pre = {}
+    for P, M, B, s_, v in t["prefill"]:
+        pre.setdefault((P, M, B), {})[s_] = unhx(v)
+    prof = SimpleNamespace(decode_table={(P, M, B): unhx(v) for P, M, B, v in t["decode"]}, prefill_table=pre,
+                           pipeline_efficiency=unhx(t["eta"]), nominal_s_in=t["nominal"][0],
+                           nominal_s_out=t["nominal"][1])
+    cands = [sk.ParallelConfig(*c) for c, _ in load("estimator")["profiles"]["gpt-20b"]["throughput"]]
+    rng = random.Random(5)
+    scen = [(rng.randint(0, 24), rng.choice([0.1, 0.25, 0.35, 0.55, 1.0, 2.0, 5.0]) * rng.uniform(0.5, 1.5),
+             rng.choice([None, rng.randint(0, 30)])) for _ in range(n_scen)]
+
+    def ours():
+        r = estimator.optimize_config_many(scen, prof, cands, 4)
+        torch.cuda.synchronize()
+        return r
+
+    got = ours()
+    t_ours = _time(ours, 3)
+    out = {"scenarios": n_scen, "candidates": len(cands), "ms": 1e3 * t_ours,
+           "decisions_per_s": n_scen / t_ours}
+    if spot:
+        from spotsim import controller as rc
+        from spotsim import costmodel as rcost
+
+        rprof = rcost.load_profile(spot.data.bundled_path("gpt-20b"))
+        rc_cands = [spot.domain.ParallelConfig(*c.as_tuple()) for c in cands]
+        k = 500
+        t0 = time.perf_counter()
+        ref = [rc.optimize_config(n, None, r, rprof, rc_cands, gpus_per_instance=4, cloud_limit=lim)
+               for n, r, lim in scen[:k]]
+        dt = time.perf_counter() - t0
+        same = sum((a is None and b is None) or (a is not None and b is not None and a.as_tuple() == b.as_tuple())
+                   for a, b in zip(got[:k], ref))
+        out.update({"reference_decisions_per_s": k / dt, "speedup": (n_scen / t_ours) / (k / dt),
+                    "checked_vs_reference": f"{same}/{k}"})
     return out
 
 
