@@ -256,8 +256,16 @@ int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages);
 int sk_exec_reset(uint32_t* d_ctl, int n_rounds, int n_stages, void* stream);
 int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_round_total, int n_rounds,
                  const int32_t* d_stage_round, int n_stages, uint32_t* d_ctl,
-                 const uint32_t* const* d_peer_progress, int n_peers, int n_ctas, double timeout_s,
-                 void* stream);
+                 const uint32_t* const* d_peer_progress, int n_peers, uint32_t* d_flag_mirror, int n_ctas,
+                 double timeout_s, void* stream);
+/* d_flag_mirror (optional): the device address of host memory (e.g. a POSIX
+ * shared-memory segment registered with sk_host_register) that receives a
+ * copy of each stage flag as it is raised -- how a consumer in ANOTHER
+ * process learns readiness without a GPU-side wait (contexts of two processes
+ * time-slice on one GPU, so a waiting consumer kernel or stream can hold off
+ * the producer). */
+int sk_host_register(void* h_ptr, uint64_t bytes, void** d_ptr);
+int sk_host_unregister(void* h_ptr);
 
 /* Consumer side of the stage-ready flags (e.g. a serving process that maps
  * a context daemon's control block with CUDA IPC): work queued on `stream`

@@ -51,7 +51,8 @@ EXPORTS = (
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
     "sk_ipc_open_handle", "sk_ipc_close_handle", "sk_fill_regions", "sk_verify_regions",
     "sk_reshard_error", "sk_migration_cost_batched", "sk_migration_cost",
-    "sk_simulate_buffer_usage", "sk_fused_elems", "sk_exec_ctl_bytes", "sk_exec_plan", "sk_exec_reset",
+    "sk_simulate_buffer_usage", "sk_fused_elems", "sk_exec_ctl_bytes", "sk_exec_plan", "sk_exec_reset", "sk_host_register",
+    "sk_host_unregister",
     "sk_memcpy_batched", "sk_d2h", "sk_wait_flag", "sk_stream_wait_flag", "sk_score_configs", "sk_select_configs",
     "sk_estimator_error", "sk_plan_migration_many",
 )

@@ -137,6 +137,7 @@ struct ExecArgs {
   const unsigned* const* peer_progress;  // every OTHER rank's progress word
   int n_peers;
   unsigned long long timeout_ns;
+  unsigned* flag_mirror;  // optional host-mapped copy of the stage flags (another process polls it)
 };
 
 __device__ __forceinline__ unsigned* exec_flags(const ExecArgs& A) { return A.ctl + 4 + A.n_rounds; }
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kX_TPB) k_exec(const ExecArgs A) {
             stamps[1 + s] = global_ns();
             __threadfence_system();
             *reinterpret_cast<volatile unsigned*>(flags + s) = 1u;
+            if (A.flag_mirror) *reinterpret_cast<volatile unsigned*>(A.flag_mirror + s) = 1u;
             --pending;
           }
         }
@@ -357,6 +359,18 @@ int sk_stream_wait_flag(const uint32_t* d_flag, uint32_t value, void* stream) {
   return SK_OK;
 }
 
+int sk_host_register(void* h_ptr, uint64_t bytes, void** d_ptr) {
+  cudaError_t e = cudaHostRegister(h_ptr, bytes, cudaHostRegisterMapped);
+  if (e != cudaSuccess) return rfail("cudaHostRegister", e);
+  e = cudaHostGetDevicePointer(d_ptr, h_ptr, 0);
+  return e == cudaSuccess ? SK_OK : rfail("cudaHostGetDevicePointer", e);
+}
+
+int sk_host_unregister(void* h_ptr) {
+  cudaError_t e = cudaHostUnregister(h_ptr);
+  return e == cudaSuccess ? SK_OK : rfail("cudaHostUnregister", e);
+}
+
 int sk_exec_reset(uint32_t* d_ctl, int n_rounds, int n_stages, void* stream) {
   const int64_t w = 4 + (int64_t)n_rounds + n_stages;
   const size_t bytes = (size_t)(((w + 1) & ~(int64_t)1) * 4 + 8 * (int64_t)(n_stages + 1));
@@ -371,8 +385,8 @@ int64_t sk_exec_ctl_bytes(int n_rounds, int n_stages) {
 
 int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_round_total, int n_rounds,
                  const int32_t* d_stage_round, int n_stages, uint32_t* d_ctl,
-                 const uint32_t* const* d_peer_progress, int n_peers, int n_ctas, double timeout_s,
-                 void* stream) {
+                 const uint32_t* const* d_peer_progress, int n_peers, uint32_t* d_flag_mirror, int n_ctas,
+                 double timeout_s, void* stream) {
   if (n_chunks < 0 || n_rounds < 0 || n_stages < 0 || n_peers < 0) {
     snprintf(g_rerr, sizeof g_rerr, "negative sizes");
     return SK_EINVAL;
@@ -389,7 +403,7 @@ int sk_exec_plan(const sk_exec_chunk* d_chunks, int n_chunks, const uint32_t* d_
     n_ctas = 2 * sms;  // two 512-thread CTAs per SM, all co-resident: the monitor + workers
   }
   ExecArgs A{d_chunks, n_chunks, d_round_total, n_rounds, d_stage_round, n_stages, d_ctl,
-             d_peer_progress, n_peers, (unsigned long long)(timeout_s * 1e9)};
+             d_peer_progress, n_peers, (unsigned long long)(timeout_s * 1e9), d_flag_mirror};
   k_exec<<<n_ctas, kX_TPB, 0, s>>>(A);
   e = cudaGetLastError();
   return e == cudaSuccess ? SK_OK : rfail("k_exec launch", e);

@@ -16,13 +16,15 @@ JSON (`plan_to_dict`, migration.py:407-431).  Here:
   per stage, the byte regions of the new context.  On `go` it runs the
   migration and answers `done` with the control block (error, rounds,
   stage-ready times) and its own byte check.
-* `DaemonClient` (the serving side) maps the slab, and per stage queues on its
-  own stream a wait on that stage's flag (`sk_stream_wait_flag`, a stream
-  memory operation: the daemon's kernels run in another context on this GPU
-  and a spinning consumer kernel could starve them) followed by the stage's
-  work -- here a byte check of the stage's context, standing in
-  for the first decode step -- so each stage starts as soon as ITS context is
-  in place, while later rounds are still moving.
+* The stage flags are mirrored by the daemon's kernel into a POSIX
+  shared-memory segment registered as mapped host memory (`sk_host_register`,
+  written with system-scope stores), because the two processes' contexts
+  time-slice on one GPU: a consumer that waits ON THE GPU (a spinning kernel,
+  or a stream semaphore wait) can hold the GPU away from the producer.
+* `DaemonClient` (the serving side) maps the slab with CUDA IPC, polls the
+  shared flags from its host thread, and launches each stage's work the moment
+  that stage's flag is up -- here a byte check of the stage's context, standing
+  in for the first decode step -- while later rounds are still moving.
 
 Messages are JSON lines.  Intervals travel as [num, den].
 """
@@ -109,6 +111,7 @@ class ContextDaemon:
 
     def _session(self, f) -> bool:
         ex = None
+        self.shm = None
         try:
             while True:
                 msg = _recv(f)
@@ -122,7 +125,7 @@ class ContextDaemon:
                     ex, reply = self._prepare(msg)
                     _send(f, reply)
                 elif op == "go":
-                    ex.run()
+                    ex.run(flag_mirror=self.mirror_dev)
                     torch.cuda.synchronize()
                     ctl = ex.control()
                     _send(f, {"op": "done", "error": ctl["error"], "progress": ctl["progress"],
@@ -133,6 +136,7 @@ class ContextDaemon:
                     if ex is not None:
                         ex.close()
                         ex = None
+                    self._drop_shm()
                     _send(f, {"op": "released"})
                     return True
                 else:
@@ -142,6 +146,16 @@ class ContextDaemon:
         finally:
             if ex is not None:
                 ex.close()
+            self._drop_shm()
+
+    def _drop_shm(self):
+        if self.shm is not None:
+            torch.cuda.synchronize()
+            ex_lib = nat.load()
+            ex_lib.sk_host_unregister(ctypes.c_void_p(self.shm_addr))
+            self.shm.close()
+            self.shm.unlink()
+            self.shm = None
 
     def _prepare(self, msg):
         model = dm.ModelSpec("wire", *msg["model"])
@@ -154,6 +168,16 @@ class ContextDaemon:
         ex.fill_old()
         ex.reset_control()   # flags down before the consumer can see the handle
         torch.cuda.synchronize()
+        # host-mapped mirror of the stage flags, shared with the consumer process
+        from multiprocessing import shared_memory
+
+        self._drop_shm()
+        self.shm = shared_memory.SharedMemory(create=True, size=max(4096, 4 * len(ex.stages)))
+        self.shm.buf[:] = bytes(len(self.shm.buf))
+        self.shm_addr = ctypes.addressof(ctypes.c_char.from_buffer(self.shm.buf))
+        d = ctypes.c_void_p()
+        nat.check(ex.lib.sk_host_register(ctypes.c_void_p(self.shm_addr), len(self.shm.buf), ctypes.byref(d)))
+        self.mirror_dev = d.value
         handle = ctypes.create_string_buffer(64)
         nat.check(ex.lib.sk_ipc_get_handle(ex.slab.ptr, handle))
         R = ex.n_rounds
@@ -167,6 +191,7 @@ class ContextDaemon:
             ptr, n, key, base = row
             regions.setdefault(str(st), []).append([ptr - ex.slab.ptr, n, str(key), base])
         return ex, {"op": "ready", "handle": handle.raw.hex(), "slab_bytes": ex.slab.nbytes,
+                    "flag_shm": self.shm.name,
                     "flag_offset": flag_off, "regions": regions, "rounds": R,
                     "stages": [int(s) for s in ex.stages]}
 
@@ -188,9 +213,13 @@ class DaemonClient:
         self.mapped = None
 
     def migrate(self, request: dict, timeout_s: float = 30.0) -> dict:
-        """Submit, map, queue the per-stage waits + checks, run.  Returns the
+        """Submit, map, run; launch each stage's work (a byte check of its new
+        context) as soon as its flag appears in the shared mirror.  Returns the
         daemon's `done` report plus, per stage, the mismatching words this
-        process saw in that stage's context right after its flag."""
+        process saw in that stage's context, and the order stages started in."""
+        import time
+        from multiprocessing import shared_memory
+
         _send(self.f, request)
         ready = _recv(self.f)
         if ready["op"] != "ready":
@@ -198,31 +227,39 @@ class DaemonClient:
         p = ctypes.c_void_p()
         nat.check(self.lib.sk_ipc_open_handle(bytes.fromhex(ready["handle"]), ctypes.byref(p)))
         self.mapped = p.value
-        st = torch.cuda.current_stream()
-        stages = ready["stages"]
-        status = torch.zeros(max(len(stages), 1), dtype=torch.int32, device="cuda")
-        bad = torch.zeros(max(len(stages), 1), dtype=torch.int64, device="cuda")
-        keep = []
-        for i, s in enumerate(stages):
-            # a stream memory op, not a spinning kernel: the daemon's kernels
-            # run in another context on this GPU and must not be starved
-            nat.check(self.lib.sk_stream_wait_flag(self.mapped + ready["flag_offset"][str(s)], 1,
-                                                   st.cuda_stream))
-            rows = ready["regions"].get(str(s), [])
-            if rows:
-                reg = np.zeros(len(rows), dtype=nat.REGION)
-                for k, (off, n, key, base) in enumerate(rows):
-                    reg[k] = (self.mapped + off, n, int(key), base)
-                d = torch.from_numpy(reg.view(np.uint8)).cuda()
-                keep.append(d)
-                nat.check(self.lib.sk_verify_regions(d.data_ptr(), len(rows), bad.data_ptr() + 8 * i,
-                                                     st.cuda_stream))
-        _send(self.f, {"op": "go"})
-        done = _recv(self.f)
-        torch.cuda.synchronize()
-        done["client_stage_mismatched_words"] = {str(s): int(b) for s, b in zip(stages, bad.tolist())}
-        done["client_wait_timeouts"] = int(status[:len(stages)].sum().item())
-        del keep
+        shm = shared_memory.SharedMemory(name=ready["flag_shm"])
+        try:
+            flags = np.ndarray((len(ready["stages"]),), dtype=np.uint32, buffer=shm.buf)
+            st = torch.cuda.current_stream()
+            stages = ready["stages"]
+            bad = torch.zeros(max(len(stages), 1), dtype=torch.int64, device="cuda")
+            keep, started = [], []
+            _send(self.f, {"op": "go"})
+            t0 = time.perf_counter()
+            pending = set(range(len(stages)))
+            while pending and time.perf_counter() - t0 < timeout_s:
+                for i in sorted(pending):
+                    if flags[i] == 0:
+                        continue
+                    pending.discard(i)
+                    started.append(stages[i])
+                    rows = ready["regions"].get(str(stages[i]), [])
+                    if rows:
+                        reg = np.zeros(len(rows), dtype=nat.REGION)
+                        for k, (off, n, key, base) in enumerate(rows):
+                            reg[k] = (self.mapped + off, n, int(key), base)
+                        d = torch.from_numpy(reg.view(np.uint8)).cuda()
+                        keep.append(d)
+                        nat.check(self.lib.sk_verify_regions(d.data_ptr(), len(rows), bad.data_ptr() + 8 * i,
+                                                             st.cuda_stream))
+            done = _recv(self.f)
+            torch.cuda.synchronize()
+            done["client_stage_mismatched_words"] = {str(s): int(b) for s, b in zip(stages, bad.tolist())}
+            done["client_wait_timeouts"] = len(pending)
+            done["client_stage_order"] = started
+            del keep, flags
+        finally:
+            shm.close()
         return done
 
     def release(self):

@@ -404,10 +404,14 @@ def _exec_lib():
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         lib.sk_exec_ctl_bytes.argtypes = [i32, i32]
         lib.sk_exec_ctl_bytes.restype = i64
-        lib.sk_exec_plan.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, i32, i32, ctypes.c_double, vp]
+        lib.sk_exec_plan.argtypes = [vp, i32, vp, i32, vp, i32, vp, vp, i32, vp, i32, ctypes.c_double, vp]
         lib.sk_exec_plan.restype = i32
         lib.sk_memcpy_batched.argtypes = [vp, i32, vp]
         lib.sk_memcpy_batched.restype = i32
+        lib.sk_host_register.argtypes = [vp, ctypes.c_uint64, ctypes.POINTER(vp)]
+        lib.sk_host_register.restype = i32
+        lib.sk_host_unregister.argtypes = [vp]
+        lib.sk_host_unregister.restype = i32
         lib.sk_exec_reset.argtypes = [vp, i32, i32, vp]
         lib.sk_exec_reset.restype = i32
         lib.sk_d2h.argtypes = [vp, vp, ctypes.c_uint64]
@@ -634,16 +638,17 @@ class ReshardExecutor:
         if n:
             nat.check(self.lib.sk_fill_regions(t.data_ptr(), n, torch.cuda.current_stream().cuda_stream))
 
-    def run(self, n_ctas: int = 0):
+    def run(self, n_ctas: int = 0, flag_mirror: int = 0):
         """The reshard: one k_exec launch over this rank's copies, in plan
         order (resets the control block first; ranks must barrier between
-        runs so no peer reads a stale progress word)."""
+        runs so no peer reads a stale progress word).  flag_mirror: device
+        address of host-mapped memory that also receives the stage flags."""
         st = torch.cuda.current_stream().cuda_stream
         nat.check(self.lib.sk_exec_plan(
             self.d_chunks.data_ptr() if self.d_chunks is not None else 0, self.n_chunks,
             self.d_totals.data_ptr() if self.d_totals is not None else 0, self.n_rounds,
             self.d_stages.data_ptr() if self.d_stages is not None else 0, len(self.stages),
-            self.slab.ptr, self.d_peers.data_ptr(), self.n_peers, n_ctas, self.timeout_s, st))
+            self.slab.ptr, self.d_peers.data_ptr(), self.n_peers, flag_mirror, n_ctas, self.timeout_s, st))
 
     def reset_control(self):
         """Zero the control block (every stage flag down) on the current stream."""
