@@ -467,21 +467,6 @@ __device__ __forceinline__ int stage_of(int x, int L, int P) {
   return x < r * (q + 1) ? x / (q + 1) : r + (x - r * (q + 1)) / q;
 }
 
-constexpr unsigned long long kRowEmpty = ~0ull;  // a NaN pattern: never a weight
-
-// row-local code of a non-zero fused weight: the first table slot holding it,
-// or the first empty one (claimed with a shared-memory CAS, so lanes racing on
-// one value agree) -> slot + 1; 0xFF when the row's table is full
-__device__ __forceinline__ unsigned row_code(unsigned long long* tab, int cap, double f) {
-  const unsigned long long v = (unsigned long long)__double_as_longlong(f);
-  for (int k = 0; k < cap; ++k) {
-    unsigned long long cur = reinterpret_cast<volatile unsigned long long*>(tab)[k];
-    if (cur == kRowEmpty) cur = atomicCAS(tab + k, kRowEmpty, v);
-    if (cur == kRowEmpty || cur == v) return (unsigned)k + 1u;
-  }
-  return 0xFFu;
-}
-
 template <int G, int LPG>
 __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
                                                  const int32_t* __restrict__ row_ptr,
@@ -489,7 +474,6 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
                                                  double* __restrict__ F, uint32_t* __restrict__ perm,
                                                  uint32_t zero_perm) {
   // LPG lanes per GPU group: small targets have few candidate slots per group
-  constexpr bool CODED = G <= 6;  // the code must fit above the 4*G perm bits
   const sk_plan p = plans[plan0 + blockIdx.y];
   if (p.group != G || (p.flags & SK_PLAN_GENERIC)) return;
   const int nA = p.rows / G;
@@ -531,117 +515,74 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   pm_over = __any_sync(kFull, pm_over);
   lo = max(lo, 0);
   hi = min(hi, p.L);
+  // the group writes its whole fused row: zeros first (coalesced, full
+  // sectors -- the encoding of an all-zero block), then the candidate blocks
   const long long row0 = p.f_off + (long long)a * nB;
-  const bool busy = live && lo < hi;  // a row group with any context
-  const int p_lo = busy ? stage_of(lo, p.L, p.P) : 0, p_hi = busy ? stage_of(hi - 1, p.L, p.P) : 0;
+  if (live) {
+    for (int b = sub; b < nB; b += LPG) {
+      F[row0 + b] = 0.0;
+      perm[row0 + b] = 0u;
+    }
+  }
+  __syncwarp();
+  if (!live || lo >= hi) return;  // the whole row group is zero
+  const int p_lo = stage_of(lo, p.L, p.P), p_hi = stage_of(hi - 1, p.L, p.P);
   const int span = ((p_hi + 1 - p_lo) * p.M) / G;  // fused slots per pipeline
   const int per_d = (p.P * p.M) / G;
   const int b0 = (p_lo * p.M) / G;
-  const int nbits = __popcll(pm0) + __popcll(pm1);
+  if (pm_over) {
+    // more pipelines than the mask tracks: every candidate block in full
+    const int total = p.D * span;
+    for (int t = sub; t < total; t += LPG) {
+      const int d = t / span;
+      const int b = d * per_d + b0 + (t - d * span);
+      const Col c0 = col_of(p, b * G);
+      const FusedBlock r = fuse_block<G>(p, a, c0, c0.d, row_ptr, segs);
+      if (r.nz) {
+        const long long idx = p.f_off + (long long)a * nB + b;
+        F[idx] = r.f;
+        perm[idx] = r.packed ^ zero_perm;
+      }
+    }
+    return;
+  }
   // work items: the model-only block of every slot offset (stored for every
   // pipeline the group's cache does not name), then the full block of every
-  // (named pipeline, offset); with more pipelines than the mask tracks, every
-  // candidate block in full
-  const int n_items = !busy ? 0 : pm_over ? p.D * span : span * (1 + nbits);
-  // Row coding (G <= 6): the row's distinct non-zero fused weights go to a
-  // per-group table (<= min(15, nB) entries, written over the head of the
-  // row's F slots) and each pair stores its 1-based table index in bits 24-31
-  // of its perm word (0 = the zero weight) -- 4 bytes per pair instead of 12,
-  // and k_outer codes the row from its table instead of hashing every weight.
-  // A row with more distinct weights falls back to plain F (code 0xFF).
-  __shared__ unsigned long long s_tab[CODED ? kF_WARPS * (32 / LPG) : 1][15];
-  unsigned long long* tab = s_tab[CODED ? (threadIdx.x >> 5) * (32 / LPG) + lane / LPG : 0];
-  const int cap = nB < 15 ? nB : 15;
-  if (CODED)
-    for (int k = sub; k < 15; k += LPG) tab[k] = kRowEmpty;
-  // the group writes its whole fused row: zeros first (coalesced, full
-  // sectors -- the encoding of an all-zero block), then the candidate blocks
-  if (live)
-    for (int b = sub; b < nB; b += LPG) {
-      if (!CODED) F[row0 + b] = 0.0;
-      perm[row0 + b] = 0u;
+  // (named pipeline, offset)
+  const int nbits = __popcll(pm0) + __popcll(pm1);
+  const int n_items = span * (1 + nbits);
+  for (int it = sub; it < n_items; it += LPG) {
+    int o = it, dq = -1;  // dq: 0-based named pipeline, -1 = model only
+    if (it >= span) {
+      const int k = (it - span) / span;
+      o = it - span - k * span;
+      // k-th set bit of the mask
+      unsigned long long m = pm0;
+      int base = 0, kk = k;
+      if (kk >= __popcll(pm0)) {
+        kk -= __popcll(pm0);
+        m = pm1;
+        base = 64;
+      }
+      for (int z = 0; z < kk; ++z) m &= m - 1;
+      dq = base + __ffsll(m) - 1;
     }
-  __syncwarp();
-  bool ovf = false;
-  // pass 0: coded (or plain F for G > 6); pass 1 (coded rows only, on table
-  // overflow): the plain-F fallback for the whole row
-  for (int pass = 0; pass < 2; ++pass) {
-    const bool plain = !CODED || pass == 1;
-    for (int it = sub; it < n_items; it += LPG) {
-      int bq, dq;  // first destination slot; dq: 0-based named pipeline, -1 = model only
-      if (pm_over) {
-        const int d = it / span;
-        bq = d * per_d + b0 + (it - d * span);
-        dq = -2;  // one destination, the block's own pipeline
-      } else {
-        int o = it;
-        dq = -1;
-        if (it >= span) {
-          const int k = (it - span) / span;
-          o = it - span - k * span;
-          // k-th set bit of the mask
-          unsigned long long m = pm0;
-          int base = 0, kk = k;
-          if (kk >= __popcll(pm0)) {
-            kk -= __popcll(pm0);
-            m = pm1;
-            base = 64;
-          }
-          for (int z = 0; z < kk; ++z) m &= m - 1;
-          dq = base + __ffsll(m) - 1;
-        }
-        bq = (dq < 0 ? 0 : dq) * per_d + b0 + o;
-      }
-      const Col c0 = col_of(p, bq * G);
-      const FusedBlock r = fuse_block<G>(p, a, c0, dq == -2 ? c0.d : dq + 1, row_ptr, segs);
-      if (!r.nz) continue;
-      uint32_t pk = r.packed ^ zero_perm;
-      if (CODED) {
-        unsigned code = 0xFFu;
-        if (!plain) {
-          code = row_code(tab, cap, r.f);
-          if (code == 0xFFu) {
-            ovf = true;
-            continue;
-          }
-        }
-        pk |= code << 24;
-      }
-      if (dq != -1) {
-        if (plain) F[row0 + bq] = r.f;
-        perm[row0 + bq] = pk;
-      } else {
-        for (int d = 0; d < p.D; ++d) {
-          const bool named = d < 64 ? ((pm0 >> d) & 1ull) : d < kF_MAXD ? ((pm1 >> (d - 64)) & 1ull) : false;
-          if (named) continue;
-          const int b = d * per_d + b0 + (bq - b0);
-          if (plain) F[row0 + b] = r.f;
-          perm[row0 + b] = pk;
-        }
+    const int bq = (dq < 0 ? 0 : dq) * per_d + b0 + o;
+    const FusedBlock r = fuse_block<G>(p, a, col_of(p, bq * G), dq + 1, row_ptr, segs);
+    if (!r.nz) continue;
+    const uint32_t pk = r.packed ^ zero_perm;
+    if (dq >= 0) {
+      F[row0 + bq] = r.f;
+      perm[row0 + bq] = pk;
+    } else {
+      for (int d = 0; d < p.D; ++d) {
+        const bool named = d < 64 ? ((pm0 >> d) & 1ull) : d < kF_MAXD ? ((pm1 >> (d - 64)) & 1ull) : false;
+        if (named) continue;
+        const int b = d * per_d + b0 + o;
+        F[row0 + b] = r.f;
+        perm[row0 + b] = pk;
       }
     }
-    if (!CODED || pass == 1) break;
-#pragma unroll
-    for (int off = LPG / 2; off; off >>= 1) ovf = ovf || __shfl_xor_sync(kFull, ovf, off);
-    if (!ovf) {
-      // the row's table over the head of its F slots (empty slots as 0.0)
-      if (live)
-        for (int k = sub; k < cap; k += LPG) {
-          const unsigned long long v = tab[k];
-          F[row0 + k] = v == kRowEmpty ? 0.0 : __longlong_as_double((long long)v);
-        }
-      break;
-    }
-    // fallback: plain F for the row, every pair marked 0xFF (only this
-    // group's lanes get here: group-masked barriers)
-    const unsigned gmask = LPG == 32 ? kFull : ((1u << LPG) - 1u) << ((lane / LPG) * LPG);
-    __syncwarp(gmask);
-    if (live)
-      for (int b = sub; b < nB; b += LPG) {
-        F[row0 + b] = 0.0;
-        perm[row0 + b] = 0xFF000000u;
-      }
-    __syncwarp(gmask);
   }
 }
 
@@ -962,25 +903,6 @@ __device__ __noinline__ double generic_pick(const double* Fp, long long nAB, int
   return Fp[nAB + e];
 }
 
-// open addressing into the plan's 256-slot dictionary, every thread for
-// itself: a plain shared load finds values already in the table (almost all
-// of them); only an empty slot takes a CAS, and racing inserts of one value
-// agree through it.  -> slot (the code); sets fail when the table is full
-__device__ __forceinline__ unsigned dict_insert(unsigned long long* table, unsigned long long bits, bool& fail) {
-  unsigned h = (unsigned)((bits * 0x9E3779B97F4A7C15ull) >> 56);
-  for (int tries = 0;; ++tries) {
-    unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(table + h);
-    if (cur == kEmpty) cur = atomicCAS(table + h, kEmpty, bits);
-    if (cur == kEmpty || cur == bits) break;
-    h = (h + 1) & (kDictSlots - 1);
-    if (tries + 1 == kDictSlots) {
-      fail = true;
-      break;
-    }
-  }
-  return h;
-}
-
 // W = warps per plan.  W == 1: one warp per plan, several plans per block,
 // warp-synchronous (the common case: many plans, small n).  W > 1: one block
 // per plan, columns spread over W warps, one __syncthreads per Dijkstra step
@@ -1042,60 +964,6 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
     for (int t = pt; t < kDictSlots; t += T) table[t] = t == 0 ? 0ull : kEmpty;
     plan_sync<W>();
     bool fail = false;
-    // row-coded plans (k_fuse with G <= 6): each row carries its <= 15
-    // distinct weights at the head of its F slots and per pair a row code in
-    // bits 24-31 of the perm word, so only the row tables are hashed and the
-    // pairs are translated through a per-row map (ucol as scratch)
-    const bool rowcoded = !dense && !(p.flags & SK_PLAN_GENERIC) && g <= 6;
-    if (rowcoded) {
-      const int cap = nB < 15 ? nB : 15;
-      const int rb = min(8, (A.dbl_elems * 8) / 16);
-      unsigned char* rmap = reinterpret_cast<unsigned char*>(ucol);
-      const uint32_t* pw = A.perm + p.f_off;
-      const float inv_n = 1.0f / (float)n;
-      for (int r0 = 0; r0 < n; r0 += rb) {
-        const int r1 = min(n, r0 + rb), rr1 = min(r1, nA);
-        for (int t = pt; t < (rr1 - r0) * cap; t += T) {
-          const int rr = t / cap, k = t - rr * cap;
-          const unsigned long long x =
-              (unsigned long long)__double_as_longlong(__ldcs(Fp + (long long)(r0 + rr) * nB + k));
-          rmap[rr * 16 + k] = (unsigned char)dict_insert(table, x, fail);
-        }
-        plan_sync<W>();
-        constexpr int U = 4;
-        const int cnt = (r1 - r0) * n;
-        for (int e0 = 0; e0 < cnt; e0 += T * U) {
-          unsigned w[U];
-          int rr[U], cc[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * T + pt;
-            int r = (int)((float)e * inv_n);
-            int c = e - r * n;
-            r = c < 0 ? r - 1 : (c >= n ? r + 1 : r);
-            c = c < 0 ? c + n : (c >= n ? c - n : c);
-            rr[u] = r;
-            cc[u] = c;
-            const bool in = e < cnt && r0 + r < nA && c < nB;
-            w[u] = in ? (__ldcs(pw + (long long)(r0 + r) * nB + c) >> 24) : (e < cnt ? 0u : 0x100u);
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (w[u] == 0x100u) continue;
-            unsigned code = 0;
-            if (w[u] == 0xFFu) {  // plain-F row
-              const unsigned long long x = (unsigned long long)__double_as_longlong(
-                  __ldcs(Fp + (long long)(r0 + rr[u]) * nB + cc[u]));
-              code = dict_insert(table, x, fail);
-            } else if (w[u] != 0u) {
-              code = rmap[rr[u] * 16 + w[u] - 1];
-            }
-            codes[(r0 + rr[u]) * n + cc[u]] = (unsigned char)code;
-          }
-        }
-        plan_sync<W>();
-      }
-    } else {
     constexpr int U = 8;  // independent loads in flight per thread
     const int cnt = n * n;  // < 2^24: exact in float
     const float inv_n = 1.0f / (float)n;
@@ -1118,30 +986,28 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       for (int u = 0; u < U; ++u) {
         const int e = e0 + u * T + pt;
         if (bits[u] == kEmpty) continue;
-        codes[e] = (unsigned char)dict_insert(table, bits[u], fail);
+        // open addressing, every thread for itself: a plain shared load finds
+        // values already in the table (almost all of them); only an empty
+        // slot takes a CAS, and racing inserts of one value agree through it
+        unsigned h = (unsigned)((bits[u] * 0x9E3779B97F4A7C15ull) >> 56);
+        for (int tries = 0;; ++tries) {
+          unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(table + h);
+          if (cur == kEmpty) cur = atomicCAS(table + h, kEmpty, bits[u]);
+          if (cur == kEmpty || cur == bits[u]) break;
+          h = (h + 1) & (kDictSlots - 1);
+          if (tries + 1 == kDictSlots) {
+            fail = true;
+            break;
+          }
+        }
+        codes[e] = (unsigned char)h;
       }
-    }
     }
     if (W == 1) {
       coded = !__any_sync(kFull, fail);
       __syncwarp();
     } else {
       coded = !__syncthreads_or(fail);
-    }
-    if (!coded && rowcoded) {
-      // more than 256 distinct weights: the cost rows come from F in L2, so
-      // decode the row-coded plan back into plain F, row by row
-      double* Fw = const_cast<double*>(Fp);
-      const int cap = nB < 15 ? nB : 15;
-      for (int r = 0; r < nA; ++r) {
-        if (pt < cap) ucol[pt] = Fp[(long long)r * nB + pt];
-        plan_sync<W>();
-        for (int c = pt; c < nB; c += T) {
-          const unsigned w = A.perm[p.f_off + (long long)r * nB + c] >> 24;
-          if (w != 0xFFu) Fw[(long long)r * nB + c] = w == 0u ? 0.0 : ucol[w - 1];
-        }
-        plan_sync<W>();
-      }
     }
   }
 
