@@ -24,7 +24,7 @@ def run_bench(*args):
 
 def test_bench_line_has_the_contract_keys():
     d = run_bench("--steps", "3", "--warmup", "3", "--positions", "64", "--sets", "16",
-                  "--cpu-seconds", "2", "--no-all-sizes")
+                  "--cpu-seconds", "2", "--no-all-sizes", "--no-dropin", "--no-k1")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
