@@ -1098,30 +1098,23 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       // fast path (~90% of steps on real plans): no negative slack and some
       // zero slack -> the minimum is 0 and the reference's j1 is the lowest
       // column whose slack is (+-)0; delta = 0 changes no potential
-      const unsigned any_neg = __ballot_sync(kFull, best < 0.0);
-      const unsigned any_zero = __ballot_sync(kFull, best == 0.0);
-      bool fast = any_neg == 0u && any_zero != 0u;
-      if (W == 1) {
-        if (fast) jw = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
-      } else {
-        // block-wide: combine the warps' (negative?, lowest zero column)
-        const unsigned zj = __reduce_min_sync(kFull, best == 0.0 ? bj : 0xffffffffu);
+      // one redux on a combined key: 0 = this lane has a negative slack,
+      // its lowest zero-slack column (1..n) if any, else all ones; the
+      // minimum is 0 (some negative: slow path), all ones (no zero: slow
+      // path), or the reference's j1 of a zero step
+      const unsigned fkey = best < 0.0 ? 0u : (best == 0.0 ? bj : 0xffffffffu);
+      unsigned fm = __reduce_min_sync(kFull, fkey);
+      if (W > 1) {
+        // block-wide: the minimum over the warps' minima
         unsigned* fp = fastx + parity * 2 * W;
-        if (lane == 0) {
-          fp[2 * pw] = any_neg != 0u;
-          fp[2 * pw + 1] = zj;
-        }
+        if (lane == 0) fp[pw] = fm;
         __syncthreads();
-        bool gneg = false;
-        unsigned gz = 0xffffffffu;
+        fm = fp[0];
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          gneg = gneg || fp[2 * w] != 0u;
-          gz = min(gz, fp[2 * w + 1]);
-        }
-        fast = !gneg && gz != 0xffffffffu;
-        if (fast) jw = gz;
+        for (int w = 1; w < W; ++w) fm = min(fm, fp[w]);
       }
+      const bool fast = fm != 0u && fm != 0xffffffffu;
+      if (fast) jw = fm;
       if (fast) {
         delta = 0.0;
       } else {
