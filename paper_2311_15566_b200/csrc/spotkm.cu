@@ -268,65 +268,81 @@ __host__ __device__ __forceinline__ void hungarian_small(const double (&w)[N][N]
 constexpr int kW_TPB = 256;
 constexpr int kW_MAXC = 2048;  // plans up to this many columns decode them once into shared memory
 constexpr int kW_RPB = 16;     // rows per block: the column table is built once per 16 rows
+constexpr int kW_SEGS = 64;    // segments of a block's rows staged in shared memory
 
 // One block per (plan, 16 rows).  The plan's column decode (stage layer block,
 // shard interval, pipeline; domain.py:92-99, 271-288) is built once into a
-// shared table, so each entry is two segment overlaps, one int -> double
-// conversion and one exact scaling -- and the row is written with coalesced
-// 16-byte stores (two adjacent columns per thread).
+// shared table and the block's row offsets and segments are staged next to it
+// in one parallel load (no dependent global load per row), then every
+// (row, column pair) of the block is one work item: two segment overlaps per
+// entry, one int -> double conversion and one exact scaling, written as
+// coalesced 16-byte stores.
 __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ plans,
                                                     const int32_t* __restrict__ row_ptr,
                                                     const sk_segment* __restrict__ segs,
                                                     double* __restrict__ W) {
   __shared__ int4 ctab[kW_MAXC];
+  __shared__ int s_rp[kW_RPB + 1];
+  __shared__ sk_segment s_seg[kW_SEGS];
   const sk_plan p = plans[blockIdx.y];
   const int r0 = blockIdx.x * kW_RPB;
   if (r0 >= p.rows) return;
-  const int r1 = min(p.rows, r0 + kW_RPB);
+  const int r1 = min(p.rows, r0 + kW_RPB), nr = r1 - r0;
   const int C = p.D * p.P * p.M;
   if ((p.flags & SK_PLAN_GENERIC) || C > kW_MAXC || p.L > 0xffff) {  // block-uniform
     const bool gen = (p.flags & SK_PLAN_GENERIC) != 0;
-    for (long long e = threadIdx.x; e < (long long)(r1 - r0) * C; e += kW_TPB) {
+    for (long long e = threadIdx.x; e < (long long)nr * C; e += kW_TPB) {
       const int r = r0 + (int)(e / C), c = (int)(e % C);
       W[p.f_off + (long long)r * C + c] = gen ? weight_generic(p, row_ptr, segs, r, c)
                                               : weight_at(p, row_ptr, segs, r, c);
     }
     return;
   }
+  if (threadIdx.x <= nr) s_rp[threadIdx.x] = row_ptr[p.row_base + r0 + threadIdx.x];
   for (int c = threadIdx.x; c < C; c += kW_TPB) {
     const Col x = col_of(p, c);
     ctab[c] = make_int4(x.s0 | (x.s1 << 16), x.i0, x.i1, x.d);
   }
   __syncthreads();
+  const int sb = s_rp[0], nseg = s_rp[nr] - sb;
+  const bool staged = nseg <= kW_SEGS;
+  if (staged)
+    for (int k = threadIdx.x; k < nseg; k += kW_TPB) s_seg[k] = segs[sb + k];
+  __syncthreads();
+  const sk_segment* sg_base = staged ? s_seg - sb : segs;
   // N / K: the exact reciprocal product when K is a power of two (bit-identical
   // to the correctly rounded division), else the IEEE division
   const bool pow2 = (p.K & (p.K - 1)) == 0;
   const double inv = 1.0 / (double)p.K;
-  for (int r = r0; r < r1; ++r) {
-    const int sb = row_ptr[p.row_base + r], se = row_ptr[p.row_base + r + 1];
-    double* out = W + p.f_off + (long long)r * C;
-    const bool vec = ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-    for (int c = 2 * threadIdx.x; c < C; c += 2 * kW_TPB) {
-      const bool two = c + 1 < C;
-      const int4 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
-      long long na = 0, nb = 0;
-      for (int k = sb; k < se; ++k) {
-        const sk_segment sg = segs[k];
-        const int la0 = max(sg.l0, ta.x & 0xffff), la1 = min(sg.l1, (int)((unsigned)ta.x >> 16));
-        const int lb0 = max(sg.l0, tb.x & 0xffff), lb1 = min(sg.l1, (int)((unsigned)tb.x >> 16));
-        const int ia = min(sg.b, ta.z) - max(sg.a, ta.y), ib = min(sg.b, tb.z) - max(sg.a, tb.y);
-        const bool pa = sg.pipe == 0 || sg.pipe == ta.w, pb = sg.pipe == 0 || sg.pipe == tb.w;
-        if (la1 > la0 && ia > 0 && pa) na += (long long)(la1 - la0) * ia * sg.unit;
-        if (lb1 > lb0 && ib > 0 && pb) nb += (long long)(lb1 - lb0) * ib * sg.unit;
-      }
-      const double wa = pow2 ? __ll2double_rn(na) * inv : num_to_w(na, p.K);
-      const double wb = pow2 ? __ll2double_rn(nb) * inv : num_to_w(nb, p.K);
-      if (two && vec) {
-        *reinterpret_cast<double2*>(out + c) = make_double2(wa, wb);
-      } else {
-        out[c] = wa;
-        if (two) out[c + 1] = wb;
-      }
+  const int cpr = (C + 1) >> 1;  // column pairs per row
+  const float inv_cpr = 1.0f / (float)cpr;
+  for (int e = threadIdx.x; e < nr * cpr; e += kW_TPB) {
+    // (row, pair) = divmod(e, cpr), exact for e < 2^24
+    int rr = (int)((float)e * inv_cpr);
+    int cp = e - rr * cpr;
+    rr = cp < 0 ? rr - 1 : (cp >= cpr ? rr + 1 : rr);
+    cp = cp < 0 ? cp + cpr : (cp >= cpr ? cp - cpr : cp);
+    const int c = 2 * cp;
+    const bool two = c + 1 < C;
+    const int4 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
+    long long na = 0, nb = 0;
+    for (int k = s_rp[rr]; k < s_rp[rr + 1]; ++k) {
+      const sk_segment sg = sg_base[k];
+      const int la0 = max(sg.l0, ta.x & 0xffff), la1 = min(sg.l1, (int)((unsigned)ta.x >> 16));
+      const int lb0 = max(sg.l0, tb.x & 0xffff), lb1 = min(sg.l1, (int)((unsigned)tb.x >> 16));
+      const int ia = min(sg.b, ta.z) - max(sg.a, ta.y), ib = min(sg.b, tb.z) - max(sg.a, tb.y);
+      const bool pa = sg.pipe == 0 || sg.pipe == ta.w, pb = sg.pipe == 0 || sg.pipe == tb.w;
+      if (la1 > la0 && ia > 0 && pa) na += (long long)(la1 - la0) * ia * sg.unit;
+      if (lb1 > lb0 && ib > 0 && pb) nb += (long long)(lb1 - lb0) * ib * sg.unit;
+    }
+    const double wa = pow2 ? __ll2double_rn(na) * inv : num_to_w(na, p.K);
+    const double wb = pow2 ? __ll2double_rn(nb) * inv : num_to_w(nb, p.K);
+    double* out = W + p.f_off + (long long)(r0 + rr) * C + c;
+    if (two && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+      *reinterpret_cast<double2*>(out) = make_double2(wa, wb);
+    } else {
+      out[0] = wa;
+      if (two) out[1] = wb;
     }
   }
 }

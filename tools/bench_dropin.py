@@ -352,7 +352,7 @@ def controller_leg(spot, n_scen: int = 20000):
     import paper_2311_15566_b200 as sk
     from paper_2311_15566_b200 import estimator
 
-    t = load("estimator")["profiles"]["gpt-20b"]
+    t = load("estimator")["profiles"]["gpt-20b"]["profile"]
     pre = {}
     for P, M, B, s_, v in t["prefill"]:
         pre.setdefault((P, M, B), {})[s_] = unhx(v)
