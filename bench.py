@@ -352,6 +352,7 @@ def measure_ours(runner, K, W, world, rank, local, flush, count_launches):
 
     for _ in range(W):
         runner.run()
+    runner.upload()   # the device-resident steps below read inputs already in HBM
     torch.cuda.synchronize()
     barrier(world)
     clocks = Clocks(local)
