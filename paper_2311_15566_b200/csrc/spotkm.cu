@@ -266,30 +266,39 @@ __host__ __device__ __forceinline__ void hungarian_small(const double (&w)[N][N]
 // K1: dense weights, two adjacent columns per thread (16-B stores)
 
 constexpr int kW_TPB = 256;
-constexpr int kW_MAXC = 2048;  // plans up to this many columns decode them once into shared memory
-constexpr int kW_RPB = 16;     // rows per block: the column table is built once per 16 rows
-constexpr int kW_SEGS = 64;    // segments of a block's rows staged in shared memory
+constexpr int kW_MAXC = 2048;  // columns decoded once into a shared table
+constexpr int kW_RPB = 16;     // rows per block
+constexpr int kW_SEGS = 32;    // segments of a block's rows staged in shared memory
+constexpr int kW_MAXPM = 64;   // stages / shards with per-segment overlap tables
 
-// One block per (plan, 16 rows).  The plan's column decode (stage layer block,
-// shard interval, pipeline; domain.py:92-99, 271-288) is built once into a
-// shared table and the block's row offsets and segments are staged next to it
-// in one parallel load (no dependent global load per row), then every
-// (row, column pair) of the block is one work item: two segment overlaps per
-// entry, one int -> double conversion and one exact scaling, written as
-// coalesced 16-byte stores.
+// One block per (plan, 16 rows).  The overlap of segment s with column
+// c = (d, st, m) factorises (domain.py:299-320): |layers(s) & stage(st)| *
+// unit(s) depends on the stage only, |[a,b) & shard(m)| on the shard only, and
+// the pipeline test on d only.  So the block builds, once, a column table
+// (st, m, d), and per staged segment the P stage products A[s][st] (int64)
+// and M shard overlaps B[s][m]; an entry is then sum_s [pipe ok] A * B -- a
+// few shared loads and one 64-bit multiply-add per segment -- converted once
+// and written with coalesced 16-byte stores.  Plans beyond the tables' sizes
+// (or general-range plans) take the per-entry path.
 __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ plans,
                                                     const int32_t* __restrict__ row_ptr,
                                                     const sk_segment* __restrict__ segs,
                                                     double* __restrict__ W) {
-  __shared__ int4 ctab[kW_MAXC];
+  __shared__ int2 ctab[kW_MAXC];
+  __shared__ long long sA[kW_SEGS][kW_MAXPM];
+  __shared__ int sB[kW_SEGS][kW_MAXPM];
+  __shared__ int sPipe[kW_SEGS];
   __shared__ int s_rp[kW_RPB + 1];
-  __shared__ sk_segment s_seg[kW_SEGS];
   const sk_plan p = plans[blockIdx.y];
   const int r0 = blockIdx.x * kW_RPB;
   if (r0 >= p.rows) return;
   const int r1 = min(p.rows, r0 + kW_RPB), nr = r1 - r0;
   const int C = p.D * p.P * p.M;
-  if ((p.flags & SK_PLAN_GENERIC) || C > kW_MAXC || p.L > 0xffff) {  // block-uniform
+  if (threadIdx.x <= nr) s_rp[threadIdx.x] = row_ptr[p.row_base + r0 + threadIdx.x];
+  __syncthreads();
+  const int sb = s_rp[0], nseg = s_rp[nr] - sb;
+  if ((p.flags & SK_PLAN_GENERIC) || C > kW_MAXC || p.P > kW_MAXPM || p.M > kW_MAXPM || nseg > kW_SEGS) {
+    // block-uniform: per-entry path
     const bool gen = (p.flags & SK_PLAN_GENERIC) != 0;
     for (long long e = threadIdx.x; e < (long long)nr * C; e += kW_TPB) {
       const int r = r0 + (int)(e / C), c = (int)(e % C);
@@ -298,18 +307,26 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
     }
     return;
   }
-  if (threadIdx.x <= nr) s_rp[threadIdx.x] = row_ptr[p.row_base + r0 + threadIdx.x];
   for (int c = threadIdx.x; c < C; c += kW_TPB) {
-    const Col x = col_of(p, c);
-    ctab[c] = make_int4(x.s0 | (x.s1 << 16), x.i0, x.i1, x.d);
+    const int m = c % p.M, t = c / p.M;
+    ctab[c] = make_int2((t % p.P) | (m << 16), t / p.P + 1);
+  }
+  const int q = p.L / p.P, rem = p.L % p.P, w = p.K / p.M;
+  for (int t = threadIdx.x; t < nseg * (p.P + p.M); t += kW_TPB) {
+    const int k = t / (p.P + p.M), x = t - k * (p.P + p.M);
+    const sk_segment sg = segs[sb + k];
+    if (x < p.P) {
+      const int s0 = x * q + min(x, rem), s1 = s0 + q + (x < rem ? 1 : 0);
+      const int ol = min(sg.l1, s1) - max(sg.l0, s0);
+      sA[k][x] = ol > 0 ? (long long)ol * sg.unit : 0ll;
+      if (x == 0) sPipe[k] = sg.pipe;
+    } else {
+      const int m = x - p.P;
+      const int oi = min(sg.b, m * w + w) - max(sg.a, m * w);
+      sB[k][m] = oi > 0 ? oi : 0;
+    }
   }
   __syncthreads();
-  const int sb = s_rp[0], nseg = s_rp[nr] - sb;
-  const bool staged = nseg <= kW_SEGS;
-  if (staged)
-    for (int k = threadIdx.x; k < nseg; k += kW_TPB) s_seg[k] = segs[sb + k];
-  __syncthreads();
-  const sk_segment* sg_base = staged ? s_seg - sb : segs;
   // N / K: the exact reciprocal product when K is a power of two (bit-identical
   // to the correctly rounded division), else the IEEE division
   const bool pow2 = (p.K & (p.K - 1)) == 0;
@@ -324,16 +341,13 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
     cp = cp < 0 ? cp + cpr : (cp >= cpr ? cp - cpr : cp);
     const int c = 2 * cp;
     const bool two = c + 1 < C;
-    const int4 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
+    const int2 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
+    const int sta = ta.x & 0xffff, ma = ta.x >> 16, stb = tb.x & 0xffff, mb = tb.x >> 16;
     long long na = 0, nb = 0;
-    for (int k = s_rp[rr]; k < s_rp[rr + 1]; ++k) {
-      const sk_segment sg = sg_base[k];
-      const int la0 = max(sg.l0, ta.x & 0xffff), la1 = min(sg.l1, (int)((unsigned)ta.x >> 16));
-      const int lb0 = max(sg.l0, tb.x & 0xffff), lb1 = min(sg.l1, (int)((unsigned)tb.x >> 16));
-      const int ia = min(sg.b, ta.z) - max(sg.a, ta.y), ib = min(sg.b, tb.z) - max(sg.a, tb.y);
-      const bool pa = sg.pipe == 0 || sg.pipe == ta.w, pb = sg.pipe == 0 || sg.pipe == tb.w;
-      if (la1 > la0 && ia > 0 && pa) na += (long long)(la1 - la0) * ia * sg.unit;
-      if (lb1 > lb0 && ib > 0 && pb) nb += (long long)(lb1 - lb0) * ib * sg.unit;
+    for (int k = s_rp[rr] - sb; k < s_rp[rr + 1] - sb; ++k) {
+      const int pipe = sPipe[k];
+      if (pipe == 0 || pipe == ta.y) na += sA[k][sta] * sB[k][ma];
+      if (pipe == 0 || pipe == tb.y) nb += sA[k][stb] * sB[k][mb];
     }
     const double wa = pow2 ? __ll2double_rn(na) * inv : num_to_w(na, p.K);
     const double wb = pow2 ? __ll2double_rn(nb) * inv : num_to_w(nb, p.K);

@@ -32,7 +32,7 @@ def main():
     a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
     b = torch.empty(n, dtype=torch.uint8, device="cuda:1")
     b.fill_(7)
-    a.zero_()
+    a.fill_(3)
     torch.cuda.synchronize(0)
     torch.cuda.synchronize(1)
     chunk = 1 << 20
@@ -53,7 +53,7 @@ def main():
             e1.record()
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
-    ok = bool((dst[:: 1 << 24] == 7).all().item())
+    ok = bool((dst[:: 1 << 24] == (7 if mode == "pull" else 3)).all().item())
     ms = min(times[1:])
     print(f"{mode} {n / 1e9:.2f} GB over NVLink: {ms:.2f} ms, {n / ms / 1e6:.1f} GB/s, bytes ok {ok}")
 
