@@ -267,19 +267,19 @@ __host__ __device__ __forceinline__ void hungarian_small(const double (&w)[N][N]
 
 constexpr int kW_TPB = 256;
 constexpr int kW_MAXC = 2048;  // columns decoded once into a shared table
-constexpr int kW_RPB = 16;     // rows per block
-constexpr int kW_SEGS = 32;    // segments of a block's rows staged in shared memory
-constexpr int kW_MAXPM = 64;   // stages / shards with per-segment overlap tables
+constexpr int kW_RPB = 64;     // rows per block (amortises the tables below)
+constexpr int kW_SEGS = 128;   // segments of a block's rows staged in shared memory
+constexpr int kW_MAXPM = 16;   // stages / shards with per-segment overlap tables
 
-// One block per (plan, 16 rows).  The overlap of segment s with column
+// One block per (plan, 64 rows).  The overlap of segment s with column
 // c = (d, st, m) factorises (domain.py:299-320): |layers(s) & stage(st)| *
 // unit(s) depends on the stage only, |[a,b) & shard(m)| on the shard only, and
 // the pipeline test on d only.  So the block builds, once, a column table
 // (st, m, d), and per staged segment the P stage products A[s][st] (int64)
 // and M shard overlaps B[s][m]; an entry is then sum_s [pipe ok] A * B -- a
-// few shared loads and one 64-bit multiply-add per segment -- converted once
-// and written with coalesced 16-byte stores.  Plans beyond the tables' sizes
-// (or general-range plans) take the per-entry path.
+// few shared loads and one 64-bit multiply-add per segment -- converted once;
+// each thread writes 4 adjacent columns (two 16-byte stores).  Plans beyond
+// the tables' sizes (or general-range plans) take the per-entry path.
 __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ plans,
                                                     const int32_t* __restrict__ row_ptr,
                                                     const sk_segment* __restrict__ segs,
@@ -312,51 +312,65 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
     ctab[c] = make_int2((t % p.P) | (m << 16), t / p.P + 1);
   }
   const int q = p.L / p.P, rem = p.L % p.P, w = p.K / p.M;
-  for (int t = threadIdx.x; t < nseg * (p.P + p.M); t += kW_TPB) {
-    const int k = t / (p.P + p.M), x = t - k * (p.P + p.M);
+  // (segment, stage) and (segment, shard) tables: thread = (k, x) over a
+  // kW_MAXPM-wide grid, so no division per item
+  for (int t = threadIdx.x; t < nseg * kW_MAXPM; t += kW_TPB) {
+    const int k = t / kW_MAXPM, x = t % kW_MAXPM;
     const sk_segment sg = segs[sb + k];
     if (x < p.P) {
       const int s0 = x * q + min(x, rem), s1 = s0 + q + (x < rem ? 1 : 0);
       const int ol = min(sg.l1, s1) - max(sg.l0, s0);
       sA[k][x] = ol > 0 ? (long long)ol * sg.unit : 0ll;
-      if (x == 0) sPipe[k] = sg.pipe;
-    } else {
-      const int m = x - p.P;
-      const int oi = min(sg.b, m * w + w) - max(sg.a, m * w);
-      sB[k][m] = oi > 0 ? oi : 0;
     }
+    if (x < p.M) {
+      const int oi = min(sg.b, x * w + w) - max(sg.a, x * w);
+      sB[k][x] = oi > 0 ? oi : 0;
+    }
+    if (x == 0) sPipe[k] = sg.pipe;
   }
   __syncthreads();
   // N / K: the exact reciprocal product when K is a power of two (bit-identical
   // to the correctly rounded division), else the IEEE division
   const bool pow2 = (p.K & (p.K - 1)) == 0;
   const double inv = 1.0 / (double)p.K;
-  const int cpr = (C + 1) >> 1;  // column pairs per row
-  const float inv_cpr = 1.0f / (float)cpr;
-  for (int e = threadIdx.x; e < nr * cpr; e += kW_TPB) {
-    // (row, pair) = divmod(e, cpr), exact for e < 2^24
-    int rr = (int)((float)e * inv_cpr);
-    int cp = e - rr * cpr;
-    rr = cp < 0 ? rr - 1 : (cp >= cpr ? rr + 1 : rr);
-    cp = cp < 0 ? cp + cpr : (cp >= cpr ? cp - cpr : cp);
-    const int c = 2 * cp;
-    const bool two = c + 1 < C;
-    const int2 ta = ctab[c], tb = two ? ctab[c + 1] : ta;
-    const int sta = ta.x & 0xffff, ma = ta.x >> 16, stb = tb.x & 0xffff, mb = tb.x >> 16;
-    long long na = 0, nb = 0;
+  constexpr int CPT = 4;  // columns per work item
+  const int ipr = (C + CPT - 1) / CPT;  // items per row
+  const float inv_ipr = 1.0f / (float)ipr;
+  for (int e = threadIdx.x; e < nr * ipr; e += kW_TPB) {
+    // (row, item) = divmod(e, ipr), exact for e < 2^24
+    int rr = (int)((float)e * inv_ipr);
+    int it = e - rr * ipr;
+    rr = it < 0 ? rr - 1 : (it >= ipr ? rr + 1 : rr);
+    it = it < 0 ? it + ipr : (it >= ipr ? it - ipr : it);
+    const int c0 = CPT * it;
+    int st[CPT], mm[CPT], dd[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+      const int2 t = ctab[min(c0 + u, C - 1)];
+      st[u] = t.x & 0xffff;
+      mm[u] = t.x >> 16;
+      dd[u] = t.y;
+    }
+    long long nu[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) nu[u] = 0;
     for (int k = s_rp[rr] - sb; k < s_rp[rr + 1] - sb; ++k) {
       const int pipe = sPipe[k];
-      if (pipe == 0 || pipe == ta.y) na += sA[k][sta] * sB[k][ma];
-      if (pipe == 0 || pipe == tb.y) nb += sA[k][stb] * sB[k][mb];
+#pragma unroll
+      for (int u = 0; u < CPT; ++u)
+        if (pipe == 0 || pipe == dd[u]) nu[u] += sA[k][st[u]] * sB[k][mm[u]];
     }
-    const double wa = pow2 ? __ll2double_rn(na) * inv : num_to_w(na, p.K);
-    const double wb = pow2 ? __ll2double_rn(nb) * inv : num_to_w(nb, p.K);
-    double* out = W + p.f_off + (long long)(r0 + rr) * C + c;
-    if (two && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-      *reinterpret_cast<double2*>(out) = make_double2(wa, wb);
+    double wv[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) wv[u] = pow2 ? __ll2double_rn(nu[u]) * inv : num_to_w(nu[u], p.K);
+    double* out = W + p.f_off + (long long)(r0 + rr) * C + c0;
+    if (c0 + CPT <= C && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+      reinterpret_cast<double2*>(out)[0] = make_double2(wv[0], wv[1]);
+      reinterpret_cast<double2*>(out)[1] = make_double2(wv[2], wv[3]);
     } else {
-      out[0] = wa;
-      if (two) out[1] = wb;
+#pragma unroll
+      for (int u = 0; u < CPT; ++u)
+        if (c0 + u < C) out[u] = wv[u];
     }
   }
 }
@@ -545,14 +559,30 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   pm_over = __any_sync(kFull, pm_over);
   lo = max(lo, 0);
   hi = min(hi, p.L);
-  // the group writes its whole fused row: zeros first (coalesced, full
-  // sectors -- the encoding of an all-zero block), then the candidate blocks
+  // the groups write their whole fused rows: zeros first (the encoding of an
+  // all-zero block), then the candidate blocks.  A warp's groups own
+  // consecutive rows, i.e. one contiguous span of F and of perm: the 32 lanes
+  // zero it together with 16-byte stores (scalar head/tail to alignment)
   const long long row0 = p.f_off + (long long)a * nB;
-  if (live) {
-    for (int b = sub; b < nB; b += LPG) {
-      F[row0 + b] = 0.0;
-      perm[row0 + b] = 0u;
-    }
+  {
+    const int a_first = a - lane / LPG;
+    const int rows_live = max(0, min(32 / LPG, nA - a_first));
+    const long long s0 = p.f_off + (long long)a_first * nB, cnt = (long long)rows_live * nB;
+    // F: doubles, 2 per 16 bytes
+    const long long fh = min(cnt, (long long)(s0 & 1));
+    if (lane < fh) F[s0 + lane] = 0.0;
+    const long long fv = (cnt - fh) >> 1;
+    double2* F2 = reinterpret_cast<double2*>(F + s0 + fh);
+    for (long long v = lane; v < fv; v += 32) F2[v] = make_double2(0.0, 0.0);
+    if (lane == 0 && ((cnt - fh) & 1)) F[s0 + cnt - 1] = 0.0;
+    // perm: uint32, 4 per 16 bytes
+    const long long ph = min(cnt, (long long)((4 - (s0 & 3)) & 3));
+    if (lane < ph) perm[s0 + lane] = 0u;
+    const long long pv = (cnt - ph) >> 2;
+    uint4* P4 = reinterpret_cast<uint4*>(perm + s0 + ph);
+    for (long long v = lane; v < pv; v += 32) P4[v] = make_uint4(0u, 0u, 0u, 0u);
+    const long long pt0 = ph + (pv << 2);
+    if (lane < cnt - pt0) perm[s0 + pt0 + lane] = 0u;
   }
   __syncwarp();
   if (!live || lo >= hi) return;  // the whole row group is zero
