@@ -153,9 +153,7 @@ int sk_map_batched(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr
 /* The two halves of sk_map_batched, for callers that time or pipeline them:
  * K2a (inner KMs + fused weights) and K2b (outer KM + expansion).  K2a
  * writes every element of each plan's fused matrix (zero rows first, then
- * only the fused pairs that can be non-zero) and the perm word of every
- * non-zero pair (a pair with F == 0.0 is an all-zero block: its permutation
- * is the zero-block one and its perm slot is left unwritten); [clear_begin, clear_begin +
+ * only the fused pairs that can be non-zero); [clear_begin, clear_begin +
  * clear_count) of d_fused / d_perm is additionally memset to zero first --
  * not needed, pass clear_count = 0.  d_steps
  * (optional, may be NULL) receives per plan {Dijkstra steps, cost-row element

@@ -561,8 +561,8 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   hi = min(hi, p.L);
   // the groups write their whole fused rows: zeros first (the encoding of an
   // all-zero block), then the candidate blocks.  A warp's groups own
-  // consecutive rows, i.e. one contiguous span of F: the 32 lanes zero it
-  // together with 16-byte stores (scalar head/tail to alignment)
+  // consecutive rows, i.e. one contiguous span of F and of perm: the 32 lanes
+  // zero it together with 16-byte stores (scalar head/tail to alignment)
   const long long row0 = p.f_off + (long long)a * nB;
   {
     const int a_first = a - lane / LPG;
@@ -575,8 +575,14 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
     double2* F2 = reinterpret_cast<double2*>(F + s0 + fh);
     for (long long v = lane; v < fv; v += 32) F2[v] = make_double2(0.0, 0.0);
     if (lane == 0 && ((cnt - fh) & 1)) F[s0 + cnt - 1] = 0.0;
-    // (perm needs no fill: the outer KM reads a pair's perm only when its
-    // fused weight is non-zero, i.e. when the block was written below)
+    // perm: uint32, 4 per 16 bytes
+    const long long ph = min(cnt, (long long)((4 - (s0 & 3)) & 3));
+    if (lane < ph) perm[s0 + lane] = 0u;
+    const long long pv = (cnt - ph) >> 2;
+    uint4* P4 = reinterpret_cast<uint4*>(perm + s0 + ph);
+    for (long long v = lane; v < pv; v += 32) P4[v] = make_uint4(0u, 0u, 0u, 0u);
+    const long long pt0 = ph + (pv << 2);
+    if (lane < cnt - pt0) perm[s0 + pt0 + lane] = 0u;
   }
   __syncwarp();
   if (!live || lo >= hi) return;  // the whole row group is zero
@@ -1267,10 +1273,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         w = Fp[nAB + e];
       } else {
         if (g > 1)
-          // (an all-zero block -- F == 0.0 exactly then -- leaves its perm slot
-          // unwritten: its permutation is the zero-block one)
-          col += (int)((((Fp[(long long)a * nB + b] == 0.0 ? 0u : A.perm[p.f_off + (long long)a * nB + b]) ^
-                         A.zero_perm[g]) >> (4 * k)) & 15u);
+          col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
         w = dense ? Fp[(long long)r * nB + col] : weight_at(p, row_ptr, segs, r, col);
       }
       out[r] = col;
@@ -1463,10 +1466,7 @@ __global__ void __launch_bounds__(kH_TPB) k_outer_huge(const OuterArgs A, unsign
         w = generic_pick(Fp, nAB, g, (long long)a * nB + b, k, &col);
       } else {
         if (g > 1)
-          // (an all-zero block -- F == 0.0 exactly then -- leaves its perm slot
-          // unwritten: its permutation is the zero-block one)
-          col += (int)((((Fp[(long long)a * nB + b] == 0.0 ? 0u : A.perm[p.f_off + (long long)a * nB + b]) ^
-                         A.zero_perm[g]) >> (4 * k)) & 15u);
+          col += (int)(((A.perm[p.f_off + (long long)a * nB + b] ^ A.zero_perm[g]) >> (4 * k)) & 15u);
         w = dense ? Fp[(long long)r * nB + col] : weight_at(p, A.row_ptr, A.segs, r, col);
       }
       out[r] = col;

@@ -125,6 +125,9 @@ class ContextDaemon:
                     ex, reply = self._prepare(msg)
                     _send(f, reply)
                 elif op == "go":
+                    if ex is None:
+                        _send(f, {"op": "error", "message": "go before migrate"})
+                        continue
                     ex.run(flag_mirror=self.mirror_dev)
                     torch.cuda.synchronize()
                     ctl = ex.control()
@@ -133,12 +136,12 @@ class ContextDaemon:
                               "stage_ready_ms": {str(k): v for k, v in ctl["stage_ready_ms"].items()},
                               "mismatched_words": ex.verify()})
                 elif op == "release":
+                    # the slab goes; the session stays open for the next plan
                     if ex is not None:
                         ex.close()
                         ex = None
                     self._drop_shm()
                     _send(f, {"op": "released"})
-                    return True
                 else:
                     _send(f, {"op": "error", "message": f"unknown op {op!r}"})
         except ConnectionError:
@@ -271,11 +274,11 @@ class DaemonClient:
         _recv(self.f)
 
     def shutdown(self):
-        _send(self.f, {"op": "shutdown"})
         try:
+            _send(self.f, {"op": "shutdown"})
             _recv(self.f)
-        except ConnectionError:
-            pass
+        except (ConnectionError, OSError):
+            pass  # the daemon already closed the session
         self.f.close()
         self.sock.close()
 
