@@ -64,6 +64,8 @@ const int64_t kKMax = (int64_t)1 << 62;   // general-range plans: K < 2^62
 const int64_t kKRegular = 0x7fffffffLL;   // regular plans: K <= 2^31 - 1
 
 PyObject* g_num = nullptr;  // interned "numerator"
+PyObject* g_num_slot = nullptr;  // interned "_numerator"
+PyObject* g_den_slot = nullptr;  // interned "_denominator"
 PyObject* g_den = nullptr;  // interned "denominator"
 
 bool as_i64(PyObject* o, int64_t* out) {
@@ -88,9 +90,18 @@ struct FracCache {
       *d = it->second.second;
       return true;
     }
-    PyObject* pn = PyObject_GetAttr(x, g_num);
-    if (!pn) return false;
-    PyObject* pd = PyObject_GetAttr(x, g_den);
+    // fractions.Fraction keeps its value in the _numerator / _denominator
+    // slots; reading them skips the Python-level properties (ints and other
+    // rationals fall back to numerator / denominator)
+    PyObject* pn = PyObject_GetAttr(x, g_num_slot);
+    PyObject* pd = pn ? PyObject_GetAttr(x, g_den_slot) : nullptr;
+    if (!pn || !pd) {
+      PyErr_Clear();
+      Py_XDECREF(pn);
+      pn = PyObject_GetAttr(x, g_num);
+      if (!pn) return false;
+      pd = PyObject_GetAttr(x, g_den);
+    }
     if (!pd) {
       Py_DECREF(pn);
       return false;
@@ -448,6 +459,8 @@ PyModuleDef kModule = {PyModuleDef_HEAD_INIT, "_hostpack", "native host-side pac
 
 PyMODINIT_FUNC PyInit__hostpack(void) {
   g_num = PyUnicode_InternFromString("numerator");
+  g_num_slot = PyUnicode_InternFromString("_numerator");
+  g_den_slot = PyUnicode_InternFromString("_denominator");
   g_den = PyUnicode_InternFromString("denominator");
   return PyModule_Create(&kModule);
 }
