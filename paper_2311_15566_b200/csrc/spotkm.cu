@@ -1106,8 +1106,12 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
 #pragma unroll
     for (int k = 0; k < CPL; ++k) minv[k] = kInf;
     int j0 = 0;
+    // (W == 1) the row whose costs the step scans is carried from the previous
+    // step's match[j0] read (match[0] = i); multi-warp shapes reload it,
+    // which keeps their register count (and occupancy) down
+    int i0c = i;
     while (true) {
-      const int i0 = match[j0];
+      const int i0 = W == 1 ? i0c : (int)match[j0];
       const double ui0 = ucol[j0];
       const unsigned act = valid & ~used;
       // the row's weights w (cost = -w; padded entries are 0.0 -> cost -0.0)
@@ -1138,6 +1142,7 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         nloads += __popc(ld);
       }
       double best = kInf;
+      unsigned bj = 0xffffffffu;  // column of the first minimum (none while best is +inf)
       int bk = 0;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
@@ -1150,9 +1155,12 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
         wr[k] = imp ? j0 : wr[k];
         const bool better = on && minv[k] < best;
         best = better ? minv[k] : best;
-        bk = better ? k : bk;
+        if (W == 1)
+          bj = better ? (unsigned)(1 + pt + T * k) : bj;
+        else
+          bk = better ? k : bk;
       }
-      const unsigned bj = (best < kInf) ? (unsigned)(1 + pt + T * bk) : 0xffffffffu;
+      if (W > 1) bj = (best < kInf) ? (unsigned)(1 + pt + T * bk) : 0xffffffffu;
       unsigned jw;
       double delta;
       // fast path (~90% of steps on real plans): no negative slack and some
@@ -1221,7 +1229,12 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
       }
       j0 = j1;
       if ((unsigned)(j0 - 1) % (unsigned)T == (unsigned)pt) used |= 1u << ((unsigned)(j0 - 1) / (unsigned)T);
-      if (match[j0] == 0) break;
+      if (W == 1) {
+        i0c = match[j0];
+        if (i0c == 0) break;
+      } else if (match[j0] == 0) {
+        break;
+      }
     }
     // every step marked one column used: the row's step count
     if (A.steps) nsteps += __popc(used);
