@@ -285,8 +285,8 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
                                                     const sk_segment* __restrict__ segs,
                                                     double* __restrict__ W) {
   __shared__ int2 ctab[kW_MAXC];
-  __shared__ long long sA[kW_SEGS][kW_MAXPM];
-  __shared__ int sB[kW_SEGS][kW_MAXPM];
+  __shared__ unsigned long long sA[kW_SEGS][kW_MAXPM];
+  __shared__ __align__(16) unsigned sB[kW_SEGS][kW_MAXPM];
   __shared__ int sPipe[kW_SEGS];
   __shared__ int s_rp[kW_RPB + 1];
   const sk_plan p = plans[blockIdx.y];
@@ -320,11 +320,11 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
     if (x < p.P) {
       const int s0 = x * q + min(x, rem), s1 = s0 + q + (x < rem ? 1 : 0);
       const int ol = min(sg.l1, s1) - max(sg.l0, s0);
-      sA[k][x] = ol > 0 ? (long long)ol * sg.unit : 0ll;
+      sA[k][x] = ol > 0 ? (unsigned long long)ol * (unsigned long long)sg.unit : 0ull;
     }
     if (x < p.M) {
       const int oi = min(sg.b, x * w + w) - max(sg.a, x * w);
-      sB[k][x] = oi > 0 ? oi : 0;
+      sB[k][x] = oi > 0 ? (unsigned)oi : 0u;
     }
     if (x == 0) sPipe[k] = sg.pipe;
   }
@@ -343,26 +343,43 @@ __global__ void __launch_bounds__(kW_TPB) k_weights(const sk_plan* __restrict__ 
     rr = it < 0 ? rr - 1 : (it >= ipr ? rr + 1 : rr);
     it = it < 0 ? it + ipr : (it >= ipr ? it - ipr : it);
     const int c0 = CPT * it;
-    int st[CPT], mm[CPT], dd[CPT];
-#pragma unroll
-    for (int u = 0; u < CPT; ++u) {
-      const int2 t = ctab[min(c0 + u, C - 1)];
-      st[u] = t.x & 0xffff;
-      mm[u] = t.x >> 16;
-      dd[u] = t.y;
-    }
-    long long nu[CPT];
+    unsigned long long nu[CPT];
 #pragma unroll
     for (int u = 0; u < CPT; ++u) nu[u] = 0;
-    for (int k = s_rp[rr] - sb; k < s_rp[rr + 1] - sb; ++k) {
-      const int pipe = sPipe[k];
+    if ((p.M & 3) == 0) {
+      // the item's 4 columns share (d, stage) and take 4 consecutive shards:
+      // per segment one stage product, one 16-byte load of shard overlaps
+      const int2 t = ctab[c0];
+      const int st = t.x & 0xffff, m0 = t.x >> 16, d = t.y;
+      for (int k = s_rp[rr] - sb; k < s_rp[rr + 1] - sb; ++k) {
+        const int pipe = sPipe[k];
+        if (pipe != 0 && pipe != d) continue;
+        const unsigned long long a = sA[k][st];
+        const uint4 b = *reinterpret_cast<const uint4*>(&sB[k][m0]);
+        nu[0] += a * b.x;
+        nu[1] += a * b.y;
+        nu[2] += a * b.z;
+        nu[3] += a * b.w;
+      }
+    } else {
+      int st[CPT], mm[CPT], dd[CPT];
 #pragma unroll
-      for (int u = 0; u < CPT; ++u)
-        if (pipe == 0 || pipe == dd[u]) nu[u] += sA[k][st[u]] * sB[k][mm[u]];
+      for (int u = 0; u < CPT; ++u) {
+        const int2 t = ctab[min(c0 + u, C - 1)];
+        st[u] = t.x & 0xffff;
+        mm[u] = t.x >> 16;
+        dd[u] = t.y;
+      }
+      for (int k = s_rp[rr] - sb; k < s_rp[rr + 1] - sb; ++k) {
+        const int pipe = sPipe[k];
+#pragma unroll
+        for (int u = 0; u < CPT; ++u)
+          if (pipe == 0 || pipe == dd[u]) nu[u] += sA[k][st[u]] * (unsigned long long)sB[k][mm[u]];
+      }
     }
     double wv[CPT];
 #pragma unroll
-    for (int u = 0; u < CPT; ++u) wv[u] = pow2 ? __ll2double_rn(nu[u]) * inv : num_to_w(nu[u], p.K);
+    for (int u = 0; u < CPT; ++u) wv[u] = pow2 ? __ull2double_rn(nu[u]) * inv : num_to_w((long long)nu[u], p.K);
     double* out = W + p.f_off + (long long)(r0 + rr) * C + c0;
     if (c0 + CPT <= C && ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
       reinterpret_cast<double2*>(out)[0] = make_double2(wv[0], wv[1]);

@@ -57,7 +57,13 @@ def test_k1_matches_exact_closed_form(n_pos, sets):
     Wh = W.cpu().numpy()
     rp_all = r.row_ptr.cpu().numpy()
     seg_all = r.segs.cpu().numpy().view(nat.SEGMENT)
-    for q in range(0, b.n_plans, max(1, b.n_plans // 6)):
+    # every 6th plan plus the first plan of each (D, P, M) shape: shard counts
+    # that are and are not multiples of 4 take different column loops in k_weights
+    qs = set(range(0, b.n_plans, max(1, b.n_plans // 6)))
+    shapes = np.stack([plans["D"], plans["P"], plans["M"]], axis=1)
+    qs |= set(np.unique(shapes, axis=0, return_index=True)[1].tolist())
+    assert {2, 4} <= set(plans["M"].tolist())
+    for q in sorted(qs):
         R, C = int(st["rows"][q]), int(st["cols"][q])
         base = int(plans["row_base"][q])
         rp = rp_all[base:base + R + 1]
