@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SPOTKM_ABI_VERSION 2
+#define SPOTKM_ABI_VERSION 3
 
 typedef enum {
   SK_OK = 0,
@@ -178,6 +178,27 @@ int sk_map_outer_codes(const sk_plan* d_plans, int n_plans, const int32_t* d_row
                        int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
                        uint8_t* d_codes, int64_t codes_bytes, void* stream);
 int64_t sk_outer_codes_bytes(int n_plans, int max_n, int max_rows);
+
+/* K2 with the fused matrix dictionary-coded by K2a itself: sk_map_fuse_coded
+ * writes each plan's fused weights as one-byte codes into the outer KM's code
+ * layout (d_codes, sk_precoded_bytes of them) and its distinct values into a
+ * 256-slot dictionary per plan (d_dict, *dict_bytes of them) instead of
+ * doubles into d_fused; sk_map_outer_coded reads them (no double matrix, no
+ * dictionary build).  A plan with more than 255 distinct non-zero fused
+ * values (and every general-range plan) still gets its double matrix in
+ * d_fused and takes the uncoded path -- same results either way.
+ * sk_precoded_bytes returns 0 when the class cannot be coded (max_n > 4095:
+ * use sk_map_fuse + sk_map_outer).  Both calls must see the same (n_plans,
+ * max_n) and buffers. */
+int64_t sk_precoded_bytes(int n_plans, int max_n, int64_t* dict_bytes);
+int sk_map_fuse_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                      const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na,
+                      int max_nb, int group_mask, uint8_t* d_codes, int64_t codes_bytes,
+                      uint64_t* d_dict, int64_t dict_bytes, void* stream);
+int sk_map_outer_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                       const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                       int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                       uint8_t* d_codes, int64_t codes_bytes, const uint64_t* d_dict, void* stream);
 /* Outer problems with n > 4095 (any size) run one 1024-thread CTA per plan
  * with the column state in device scratch that the call allocates
  * stream-ordered (cudaMallocAsync) and frees on the same stream. */

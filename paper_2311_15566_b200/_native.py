@@ -20,7 +20,7 @@ SK_OK, SK_EINVAL, SK_EGROUP, SK_ERANGE, SK_ENOSOURCE, SK_ECUDA, SK_ENOPEER = ran
 SK_PLAN_FUSED_SUM = 1
 SK_PLAN_DENSE = 2
 SK_PLAN_GENERIC = 4
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_GENERIC_GROUP = 32   # k_fuse_generic: one warp per fused pair
 
 # numpy mirrors of the C structs (field order and sizes must match spotkm.h)
@@ -46,6 +46,7 @@ assert SEGMENT.itemsize == 32 and PLAN.itemsize == 64 and SWEEP_DESC.itemsize ==
 EXPORTS = (
     "sk_abi_version", "sk_last_error", "sk_build_weights", "sk_map_batched", "sk_map_fuse",
     "sk_map_outer", "sk_map_outer_codes", "sk_outer_codes_bytes", "sk_km_dense",
+    "sk_precoded_bytes", "sk_map_fuse_coded", "sk_map_outer_coded",
     "sk_sweep_expand", "sk_copy_batched", "sk_enable_peer_access",
     "sk_plan_migration", "sk_mig_counts", "sk_mig_export", "sk_mig_free", "sk_planner_error",
     "sk_plan_timeline", "sk_memopt_order", "sk_dev_alloc", "sk_dev_free", "sk_ipc_get_handle",
@@ -90,6 +91,9 @@ def load():
         "sk_map_outer": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp], i32),
         "sk_map_outer_codes": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i64, vp], i32),
         "sk_outer_codes_bytes": ([i32, i32, i32], i64),
+        "sk_precoded_bytes": ([i32, i32, ctypes.POINTER(i64)], i64),
+        "sk_map_fuse_coded": ([vp, i32, vp, vp, vp, vp, i32, i32, i32, vp, i64, vp, i64, vp], i32),
+        "sk_map_outer_coded": ([vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i64, vp, vp], i32),
         "sk_km_dense": ([vp, i32, vp, vp, vp, i32, i32, vp], i32),
         "sk_fused_elems": ([i32, i32, i32, i32], i64),
         "sk_sweep_expand": ([vp, i32, vp, vp, vp, vp, vp, i32, vp], i32),

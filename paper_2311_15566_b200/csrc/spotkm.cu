@@ -497,6 +497,52 @@ __device__ __forceinline__ FusedBlock fuse_block(const sk_plan& p, int a, const 
   return out;
 }
 
+// dictionary coding of fused values: 256 one-byte codes per plan; code 0 is
+// +0.0 (the zero fill); kEmpty marks a free slot
+constexpr int kDictSlots = 256;
+constexpr unsigned long long kEmpty = ~0ull;  // a NaN pattern: never a weight
+
+// k_fuse's code output (CODES mode): per class-local plan q the zero-padded
+// n x n code matrix at codes + q * stride + 16 (k_outer's global-code layout)
+// and the 256-slot dictionary at dict + q * 256 (slot 0: overflow flag, kEmpty
+// while the plan's values fit)
+struct FuseCodes {
+  unsigned char* codes;
+  size_t stride;
+  unsigned long long* dict;
+};
+
+// the code of fused value f in the plan's dictionary: open addressing over
+// slots 1..255 of the global table (write-once slots, claimed by CAS), with a
+// per-CTA shared-memory mirror so repeated values cost one shared load (the
+// probe that misses the mirror is out of line)
+__device__ __noinline__ unsigned fuse_code_slow(unsigned long long x, unsigned h, unsigned long long* s_dict,
+                                                unsigned long long* g_dict) {
+  volatile unsigned long long* sd = s_dict;
+  for (int tries = 0; tries < kDictSlots; ++tries, h = (h + 1) & (kDictSlots - 1)) {
+    if (h == 0) continue;
+    unsigned long long c = sd[h];
+    if (c == kEmpty) c = __ldcg(g_dict + h);  // usually claimed by another CTA already
+    if (c == kEmpty) {
+      c = atomicCAS(g_dict + h, kEmpty, x);
+      if (c == kEmpty) c = x;
+    }
+    sd[h] = c;
+    if (c == x) return h;
+  }
+  g_dict[0] = 0ull;  // overflow: the plan takes the uncoded path
+  return 0;
+}
+
+__device__ __forceinline__ unsigned char fuse_code(double f, unsigned long long* s_dict,
+                                                   unsigned long long* g_dict) {
+  const unsigned long long x = (unsigned long long)__double_as_longlong(f);
+  if (x == 0ull) return 0;
+  const unsigned h = (unsigned)((x * 0x9E3779B97F4A7C15ull) >> 56);
+  if (h != 0 && *reinterpret_cast<volatile unsigned long long*>(s_dict + h) == x) return (unsigned char)h;
+  return (unsigned char)fuse_code_slow(x, h, s_dict, g_dict);
+}
+
 // One lane group (LPG lanes) per fused GPU group a.  The group first writes
 // its whole fused row as zeros (F = 0.0, perm = 0 meaning "zero-matrix
 // permutation"; coalesced full sectors, no separate clear and no partial-
@@ -528,19 +574,19 @@ __device__ __forceinline__ int stage_of(int x, int L, int P) {
   return x < r * (q + 1) ? x / (q + 1) : r + (x - r * (q + 1)) / q;
 }
 
-template <int G, int LPG>
-__global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
-                                                 const int32_t* __restrict__ row_ptr,
-                                                 const sk_segment* __restrict__ segs,
-                                                 double* __restrict__ F, uint32_t* __restrict__ perm,
-                                                 uint32_t zero_perm) {
+template <int G, int LPG, bool CODES>
+__device__ __forceinline__ void fuse_rows(const sk_plan& p, int q, int bx,
+                                          const int32_t* __restrict__ row_ptr,
+                                          const sk_segment* __restrict__ segs,
+                                          double* __restrict__ F, uint32_t* __restrict__ perm,
+                                          uint32_t zero_perm, const FuseCodes& fc,
+                                          unsigned long long* s_dict) {
   // LPG lanes per GPU group: small targets have few candidate slots per group
-  const sk_plan p = plans[plan0 + blockIdx.y];
-  if (p.group != G || (p.flags & SK_PLAN_GENERIC)) return;
   const int nA = p.rows / G;
   const int nB = (p.D * p.P * p.M) / G;
+  const int n = nA > nB ? nA : nB;
   const int lane = threadIdx.x & 31, sub = lane % LPG;
-  const int a = (blockIdx.x * kF_WARPS + (threadIdx.x >> 5)) * (32 / LPG) + lane / LPG;
+  const int a = (bx * kF_WARPS + (threadIdx.x >> 5)) * (32 / LPG) + lane / LPG;
   const bool live = a < nA;
   int lo = 0x7fffffff, hi = -1;
   unsigned long long pm0 = 0, pm1 = 0;  // cache pipelines 1..128 named by the group
@@ -581,17 +627,34 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
   // consecutive rows, i.e. one contiguous span of F and of perm: the 32 lanes
   // zero it together with 16-byte stores (scalar head/tail to alignment)
   const long long row0 = p.f_off + (long long)a * nB;
+  // CODES: the plan's zero-padded n x n one-byte code matrix (k_outer's layout)
+  unsigned char* const crow = CODES ? fc.codes + (size_t)q * fc.stride + 16 + (size_t)a * n : nullptr;
   {
     const int a_first = a - lane / LPG;
     const int rows_live = max(0, min(32 / LPG, nA - a_first));
     const long long s0 = p.f_off + (long long)a_first * nB, cnt = (long long)rows_live * nB;
-    // F: doubles, 2 per 16 bytes
-    const long long fh = min(cnt, (long long)(s0 & 1));
-    if (lane < fh) F[s0 + lane] = 0.0;
-    const long long fv = (cnt - fh) >> 1;
-    double2* F2 = reinterpret_cast<double2*>(F + s0 + fh);
-    for (long long v = lane; v < fv; v += 32) F2[v] = make_double2(0.0, 0.0);
-    if (lane == 0 && ((cnt - fh) & 1)) F[s0 + cnt - 1] = 0.0;
+    if (CODES) {
+      // code 0 (+0.0) over the warp's rows of the n x n matrix, padding rows
+      // nA..n-1 and columns nB..n-1 included
+      const int crows = max(0, min(32 / LPG, n - a_first));
+      unsigned char* c0p = fc.codes + (size_t)q * fc.stride + 16 + (size_t)a_first * n;
+      const long long ccnt = (long long)crows * n;
+      const long long ch = min(ccnt, (long long)((16 - (reinterpret_cast<uintptr_t>(c0p) & 15)) & 15));
+      if (lane < ch) c0p[lane] = 0;
+      const long long cv = (ccnt - ch) >> 4;
+      uint4* C4 = reinterpret_cast<uint4*>(c0p + ch);
+      for (long long v = lane; v < cv; v += 32) C4[v] = make_uint4(0u, 0u, 0u, 0u);
+      const long long ct0 = ch + (cv << 4);
+      if (lane < ccnt - ct0) c0p[ct0 + lane] = 0;
+    } else {
+      // F: doubles, 2 per 16 bytes
+      const long long fh = min(cnt, (long long)(s0 & 1));
+      if (lane < fh) F[s0 + lane] = 0.0;
+      const long long fv = (cnt - fh) >> 1;
+      double2* F2 = reinterpret_cast<double2*>(F + s0 + fh);
+      for (long long v = lane; v < fv; v += 32) F2[v] = make_double2(0.0, 0.0);
+      if (lane == 0 && ((cnt - fh) & 1)) F[s0 + cnt - 1] = 0.0;
+    }
     // perm: uint32, 4 per 16 bytes
     const long long ph = min(cnt, (long long)((4 - (s0 & 3)) & 3));
     if (lane < ph) perm[s0 + lane] = 0u;
@@ -617,7 +680,10 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
       const FusedBlock r = fuse_block<G>(p, a, c0, c0.d, row_ptr, segs);
       if (r.nz) {
         const long long idx = p.f_off + (long long)a * nB + b;
-        F[idx] = r.f;
+        if (CODES)
+          crow[b] = fuse_code(r.f, s_dict, fc.dict + (size_t)q * kDictSlots);
+        else
+          F[idx] = r.f;
         perm[idx] = r.packed ^ zero_perm;
       }
     }
@@ -648,18 +714,79 @@ __global__ void __launch_bounds__(kF_TPB) k_fuse(const sk_plan* __restrict__ pla
     const FusedBlock r = fuse_block<G>(p, a, col_of(p, bq * G), dq + 1, row_ptr, segs);
     if (!r.nz) continue;
     const uint32_t pk = r.packed ^ zero_perm;
+    unsigned char code = 0;
+    if (CODES) code = fuse_code(r.f, s_dict, fc.dict + (size_t)q * kDictSlots);
     if (dq >= 0) {
-      F[row0 + bq] = r.f;
+      if (CODES)
+        crow[bq] = code;
+      else
+        F[row0 + bq] = r.f;
       perm[row0 + bq] = pk;
     } else {
       for (int d = 0; d < p.D; ++d) {
         const bool named = d < 64 ? ((pm0 >> d) & 1ull) : d < kF_MAXD ? ((pm1 >> (d - 64)) & 1ull) : false;
         if (named) continue;
         const int b = d * per_d + b0 + o;
-        F[row0 + b] = r.f;
+        if (CODES)
+          crow[b] = code;
+        else
+          F[row0 + b] = r.f;
         perm[row0 + b] = pk;
       }
     }
+  }
+}
+
+#ifndef SK_FC_MINB
+#define SK_FC_MINB 6
+#endif
+template <int G, int LPG, bool CODES>
+__global__ void __launch_bounds__(kF_TPB, CODES && G <= 4 ? SK_FC_MINB : 1) k_fuse(const sk_plan* __restrict__ plans, int plan0,
+                                                 const int32_t* __restrict__ row_ptr,
+                                                 const sk_segment* __restrict__ segs,
+                                                 double* __restrict__ F, uint32_t* __restrict__ perm,
+                                                 uint32_t zero_perm, const FuseCodes fc) {
+  const int q = plan0 + blockIdx.y;
+  const sk_plan p = plans[q];
+  if (p.group != G || (p.flags & SK_PLAN_GENERIC)) return;
+  __shared__ unsigned long long s_dict[CODES ? kDictSlots : 1];
+  if (CODES) {
+    for (int t = threadIdx.x; t < kDictSlots; t += kF_TPB) s_dict[t] = kEmpty;
+    __syncthreads();
+  }
+  fuse_rows<G, LPG, CODES>(p, q, blockIdx.x, row_ptr, segs, F, perm, zero_perm, fc, s_dict);
+}
+
+// After a CODES pass: the plans whose fused values overflowed the 255-entry
+// dictionary (its slot 0 set) get their fused rows as doubles, for the outer
+// KM's uncoded path.  A few CTAs walk all plans; the rest exit at the flag.
+template <int G>
+__global__ void __launch_bounds__(kF_TPB) k_fuse_overflow(const sk_plan* __restrict__ plans, int n_plans,
+                                                          const int32_t* __restrict__ row_ptr,
+                                                          const sk_segment* __restrict__ segs,
+                                                          double* __restrict__ F, uint32_t* __restrict__ perm,
+                                                          uint32_t zero_perm, const FuseCodes fc) {
+  constexpr int kGroupsPerBlock = kF_WARPS * (32 / 4);
+  __shared__ int s_list[kF_TPB];
+  __shared__ int s_cnt;
+  for (int q0 = blockIdx.x * kF_TPB; q0 < n_plans; q0 += gridDim.x * kF_TPB) {
+    // one flag per thread, the overflowed plans of G listed in shared memory
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    const int q = q0 + threadIdx.x;
+    if (q < n_plans && __ldcg(fc.dict + (size_t)q * kDictSlots) != kEmpty && plans[q].group == G &&
+        !(plans[q].flags & SK_PLAN_GENERIC))
+      s_list[atomicAdd(&s_cnt, 1)] = q;
+    __syncthreads();
+    const int cnt = s_cnt;
+    for (int i = 0; i < cnt; ++i) {
+      const int qq = s_list[i];
+      const sk_plan p = plans[qq];
+      const int nbx = (p.rows / G + kGroupsPerBlock - 1) / kGroupsPerBlock;
+      for (int bx = 0; bx < nbx; ++bx)
+        fuse_rows<G, 4, false>(p, qq, bx, row_ptr, segs, F, perm, zero_perm, fc, nullptr);
+    }
+    __syncthreads();
   }
 }
 
@@ -704,16 +831,35 @@ int launch_fuse(const sk_plan* d_plans, int p0, int np, int max_na, int max_nb, 
   dim3 grid((max_na + groups_per_block - 1) / groups_per_block, np);
   const uint32_t zp = zero_perm_of(G);
   if (lpg == 2)
-    k_fuse<G, 2><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+    k_fuse<G, 2, false><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp, FuseCodes{});
   else if (lpg == 4)
-    k_fuse<G, 4><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+    k_fuse<G, 4, false><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp, FuseCodes{});
   else if (lpg == 8)
-    k_fuse<G, 8><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+    k_fuse<G, 8, false><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp, FuseCodes{});
   else if (lpg == 16)
-    k_fuse<G, 16><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+    k_fuse<G, 16, false><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp, FuseCodes{});
   else
-    k_fuse<G, 32><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp);
+    k_fuse<G, 32, false><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, F, perm, zp, FuseCodes{});
   return cuda_check("k_fuse launch");
+}
+
+template <int G>
+int launch_fuse_coded(const sk_plan* d_plans, int p0, int np, int max_n, const int32_t* row_ptr,
+                      const sk_segment* segs, uint32_t* perm, const FuseCodes& fc, cudaStream_t s) {
+  constexpr int kGroupsPerBlock = kF_WARPS * (32 / 4);
+  dim3 grid((max_n + kGroupsPerBlock - 1) / kGroupsPerBlock, np);
+  k_fuse<G, 4, true><<<grid, kF_TPB, 0, s>>>(d_plans, p0, row_ptr, segs, nullptr, perm, zero_perm_of(G), fc);
+  return cuda_check("k_fuse (coded) launch");
+}
+
+template <int G>
+int launch_fuse_overflow(const sk_plan* d_plans, int n_plans, const int32_t* row_ptr,
+                         const sk_segment* segs, double* F, uint32_t* perm, const FuseCodes& fc,
+                         cudaStream_t s) {
+  const int need = (n_plans + kF_TPB - 1) / kF_TPB;
+  const int ctas = need < 148 * 4 ? need : 148 * 4;
+  k_fuse_overflow<G><<<ctas, kF_TPB, 0, s>>>(d_plans, n_plans, row_ptr, segs, F, perm, zero_perm_of(G), fc);
+  return cuda_check("k_fuse_overflow launch");
 }
 
 // ---------------------------------------------------------------------------
@@ -892,8 +1038,6 @@ __host__ __device__ __forceinline__ int outer_dbl_elems(int max_n, int max_rows,
 // nA x nB matrix into one-byte codes + a 256-entry table in shared memory and
 // every Dijkstra step gathers its cost row from shared memory instead of L2.
 // A plan with more than 256 distinct values falls back to the L2 gather.
-constexpr int kDictSlots = 256;
-constexpr unsigned long long kEmpty = ~0ull;  // a NaN pattern: never a weight
 
 // match / way are int16 (n <= 4095)
 __host__ __device__ __forceinline__ size_t outer_base_bytes(int max_n, int dbl_elems) {
@@ -942,6 +1086,9 @@ struct OuterArgs {
   int wv_in_dict;  // coded modes: epilogue row weights live in the dictionary area
   unsigned char* codes;  // kOuterGlobalCodes: per plan q at codes + q * codes_stride + 16
   size_t codes_stride;
+  // optional: k_fuse's dictionaries (FuseCodes); a plan whose slot 0 is still
+  // kEmpty arrives coded (codes as above, in every mode) -- no build from F
+  const unsigned long long* dict;
 };
 
 // per-plan stride of the global code scratch: a 16-byte head (the step's
@@ -1036,7 +1183,24 @@ __global__ void __launch_bounds__(32 * (W > kO_WARPS ? W : kO_WARPS)) k_outer(co
   Partial* partial = reinterpret_cast<Partial*>(
       base + (A.smem_per_warp - (size_t)2 * W * sizeof(Partial)));
   unsigned* fastx = reinterpret_cast<unsigned*>(partial) - 4 * W;  // [2][W] x {neg, zero j}
-  if (CODED) {
+  const bool precoded = CODED && A.dict != nullptr && !(p.flags & SK_PLAN_GENERIC) &&
+                        __ldcg(A.dict + (size_t)q * kDictSlots) == kEmpty;
+  if (precoded) {
+    // k_fuse coded the plan: its dictionary into shared memory (+ the codes
+    // themselves in the shared-memory mode; the global mode reads them in place)
+    const unsigned long long* gd = A.dict + (size_t)q * kDictSlots;
+    for (int t = pt; t < kDictSlots; t += T) table[t] = t == 0 ? 0ull : __ldcg(gd + t);
+    if (MODE == kOuterSmemCodes) {
+      // whole 16-byte words: the tail read stays inside the plan's stride and
+      // the tail write inside the shared slack
+      const uint4* src = reinterpret_cast<const uint4*>(A.codes + (size_t)q * A.codes_stride + 16);
+      uint4* dst = reinterpret_cast<uint4*>(codes);
+      const int c16 = (n * n + 15) >> 4;
+      for (int e = pt; e < c16; e += T) dst[e] = __ldcs(src + e);
+    }
+    plan_sync<W>();
+    coded = true;
+  } else if (CODED) {
     // slot 0 holds +0.0 (its own hash slot), the code of the zero padding
     for (int t = pt; t < kDictSlots; t += T) table[t] = t == 0 ? 0ull : kEmpty;
     plan_sync<W>();
@@ -1826,6 +1990,73 @@ int sk_map_fuse(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
     if (rc) return rc;
   }
   return SK_OK;
+}
+
+int64_t sk_precoded_bytes(int n_plans, int max_n, int64_t* dict_bytes) {
+  if (dict_bytes) *dict_bytes = 0;
+  if (n_plans <= 0 || max_n <= 0 || max_n > 4095) return 0;
+  int cpl = 0, w = 0;
+  outer_shape(max_n, &cpl, &w);
+  if (dict_bytes) *dict_bytes = (int64_t)n_plans * kDictSlots * 8;
+  return (int64_t)(outer_codes_stride(max_n, w, cpl) * (size_t)n_plans);
+}
+
+int sk_map_fuse_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                      const sk_segment* d_segs, double* d_fused, uint32_t* d_perm, int max_na,
+                      int max_nb, int group_mask, uint8_t* d_codes, int64_t codes_bytes,
+                      uint64_t* d_dict, int64_t dict_bytes, void* stream) {
+  if (n_plans < 0 || max_na < 0 || max_nb < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0 || max_na == 0 || max_nb == 0) return SK_OK;
+  const int max_n = max_na > max_nb ? max_na : max_nb;
+  int64_t need_dict = 0;
+  const int64_t need = sk_precoded_bytes(n_plans, max_n, &need_dict);
+  if (need == 0 || d_codes == nullptr || d_dict == nullptr || codes_bytes < need || dict_bytes < need_dict)
+    return set_err(SK_EINVAL, "coded fuse: code scratch %lld B / dictionaries %lld B needed (max_n %d)",
+                   (long long)need, (long long)need_dict, max_n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(d_dict, 0xff, (size_t)need_dict, s) != cudaSuccess) return cuda_check("clear dictionaries");
+  int cpl = 0, w = 0;
+  outer_shape(max_n, &cpl, &w);
+  const FuseCodes fc{d_codes, outer_codes_stride(max_n, w, cpl), reinterpret_cast<unsigned long long*>(d_dict)};
+  const int mask = group_mask ? group_mask : 0x1ff;
+  for (int p0 = 0; p0 < n_plans; p0 += kMaxGridY) {
+    const int np = n_plans - p0 < kMaxGridY ? n_plans - p0 : kMaxGridY;
+    int rc = SK_OK;
+    if (mask & 1) {  // general-range plans keep the double matrix (the outer KM codes them itself)
+      const long long pairs = (long long)max_na * max_nb;
+      if ((pairs + kG_WARPS - 1) / kG_WARPS > 0x7fffffffLL) return set_err(SK_EINVAL, "too many fused pairs");
+      dim3 grid((unsigned)((pairs + kG_WARPS - 1) / kG_WARPS), np);
+      k_fuse_generic<<<grid, 32 * kG_WARPS, 0, s>>>(d_plans, p0, d_row_ptr, d_segs, d_fused);
+      rc = cuda_check("k_fuse_generic launch");
+    }
+#define SK_FUSE_CODED(GG) \
+    if (!rc && (mask & (1 << GG))) rc = launch_fuse_coded<GG>(d_plans, p0, np, max_n, d_row_ptr, d_segs, d_perm, fc, s);
+    SK_FUSE_CODED(1) SK_FUSE_CODED(2) SK_FUSE_CODED(3) SK_FUSE_CODED(4)
+    SK_FUSE_CODED(5) SK_FUSE_CODED(6) SK_FUSE_CODED(7) SK_FUSE_CODED(8)
+#undef SK_FUSE_CODED
+    if (rc) return rc;
+  }
+  int rc = SK_OK;
+#define SK_FUSE_OVF(GG) \
+  if (!rc && (mask & (1 << GG))) rc = launch_fuse_overflow<GG>(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, fc, s);
+  SK_FUSE_OVF(1) SK_FUSE_OVF(2) SK_FUSE_OVF(3) SK_FUSE_OVF(4)
+  SK_FUSE_OVF(5) SK_FUSE_OVF(6) SK_FUSE_OVF(7) SK_FUSE_OVF(8)
+#undef SK_FUSE_OVF
+  return rc;
+}
+
+int sk_map_outer_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,
+                       const sk_segment* d_segs, const double* d_fused, const uint32_t* d_perm,
+                       int32_t* d_assign, double* d_total, int64_t* d_steps, int max_n, int max_rows,
+                       uint8_t* d_codes, int64_t codes_bytes, const uint64_t* d_dict, void* stream) {
+  if (n_plans < 0 || max_n < 0 || max_rows < 0 || codes_bytes < 0) return set_err(SK_EINVAL, "negative sizes");
+  if (n_plans == 0) return SK_OK;
+  if (sk_precoded_bytes(n_plans, max_n, nullptr) > codes_bytes || d_codes == nullptr || d_dict == nullptr)
+    return set_err(SK_EINVAL, "coded outer KM: code scratch too small");
+  OuterArgs A{d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, d_assign, d_total, d_steps, {}, 0, max_n, 0,
+              0, d_codes, 0, reinterpret_cast<const unsigned long long*>(d_dict)};
+  for (int g = 0; g <= 8; ++g) A.zero_perm[g] = zero_perm_of(g);
+  return outer_dispatch(A, max_rows, (size_t)codes_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int sk_map_outer_codes(const sk_plan* d_plans, int n_plans, const int32_t* d_row_ptr,

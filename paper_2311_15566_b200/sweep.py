@@ -17,6 +17,7 @@ inheritance on min(D_old, D_new).
 
 from __future__ import annotations
 
+import ctypes
 import os
 from dataclasses import dataclass
 from math import lcm
@@ -243,11 +244,24 @@ class SweepRunner:
                            for a, b, _ in self.classes]
         # global code scratch for the big size classes (sk_outer_codes_bytes);
         # the classes run concurrently, so each gets its own slice
-        need = [int(self.lib.sk_outer_codes_bytes(b - a, mn, rows))
-                for (a, b, mn), rows in zip(self.classes, self.class_rows)]
+        # coded K2 (default; SK_PRECODED=0 disables, for A/B): k_fuse writes
+        # one-byte codes + a per-plan dictionary instead of the double matrix,
+        # so every codable class needs the code scratch and dictionaries
+        self.precoded = os.environ.get("SK_PRECODED", "1") != "0"
+        need, dneed, coded = [], [], []
+        for (a, b, mn), rows in zip(self.classes, self.class_rows):
+            d = ctypes.c_int64(0)
+            pc = int(self.lib.sk_precoded_bytes(b - a, mn, ctypes.byref(d))) if self.precoded else 0
+            coded.append(pc > 0)
+            need.append(pc if pc > 0 else int(self.lib.sk_outer_codes_bytes(b - a, mn, rows)))
+            dneed.append(int(d.value) if pc > 0 else 0)
+        self.class_coded = coded
         self.codes_off = np.concatenate([[0], np.cumsum(need)]).astype(np.int64)
         self.codes_need = need
         self.codes = buf("codes", max(int(self.codes_off[-1]), 1), torch.uint8)
+        self.dict_off = np.concatenate([[0], np.cumsum(dneed)]).astype(np.int64)
+        self.dict_need = dneed
+        self.dict = buf("dict", max(int(self.dict_off[-1]) // 8, 1), torch.int64)
         self.stream = stream
         # one side stream per outer-KM size class so the classes' tails overlap
         self.side = [torch.cuda.Stream(self.dev) for _ in self.classes]
@@ -317,19 +331,27 @@ class SweepRunner:
                                               self.class_rows[c], st.cuda_stream)
                 nat.check(rc)
                 mark(f"k_sweep_expand[{c}]")
-            rc = self.lib.sk_map_fuse(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
-                                      self.segs.data_ptr(), self.fused.data_ptr(),
-                                      self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
-                                      self.class_gmask[c], 0, 0, st.cuda_stream)
+            codes = self.codes.data_ptr() + int(self.codes_off[c])
+            dct = self.dict.data_ptr() + int(self.dict_off[c])
+            if self.class_coded[c]:
+                rc = self.lib.sk_map_fuse_coded(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
+                                                self.segs.data_ptr(), self.fused.data_ptr(),
+                                                self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
+                                                self.class_gmask[c], codes, self.codes_need[c], dct,
+                                                self.dict_need[c], st.cuda_stream)
+            else:
+                rc = self.lib.sk_map_fuse(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
+                                          self.segs.data_ptr(), self.fused.data_ptr(),
+                                          self.perm.data_ptr(), self.class_na[c], self.class_nb[c],
+                                          self.class_gmask[c], 0, 0, st.cuda_stream)
             nat.check(rc)
             mark(f"k_fuse[{c}]")
-            rc = self.lib.sk_map_outer_codes(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(),
-                                             self.segs.data_ptr(), self.fused.data_ptr(),
-                                             self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
-                                             0 if steps is None else steps.data_ptr() + 16 * a, mn,
-                                             self.class_rows[c],
-                                             self.codes.data_ptr() + int(self.codes_off[c]),
-                                             self.codes_need[c], st.cuda_stream)
+            outer = self.lib.sk_map_outer_coded if self.class_coded[c] else self.lib.sk_map_outer_codes
+            extra = (dct,) if self.class_coded[c] else ()
+            rc = outer(p_plans + 64 * a, b - a, self.row_ptr.data_ptr(), self.segs.data_ptr(),
+                       self.fused.data_ptr(), self.perm.data_ptr(), out + 8 * Q, out + 8 * a,
+                       0 if steps is None else steps.data_ptr() + 16 * a, mn, self.class_rows[c],
+                       codes, self.codes_need[c], *extra, st.cuda_stream)
             nat.check(rc)
             mark(f"k_outer[{c}]")
             if download:

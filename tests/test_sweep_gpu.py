@@ -121,3 +121,33 @@ def test_forced_global_codes_all_shapes_match_c_oracle(n_pos):
                          text=True, timeout=900)
     assert res.returncode == 0, res.stderr[-3000:]
     assert res.stdout.startswith("ok")
+
+
+def test_coded_fuse_overflow_and_stale_scratch():
+    """k_fuse codes the fused matrix itself (sk_map_fuse_coded): plans with
+    more than 255 distinct fused values overflow their dictionary and take the
+    double-matrix path; stale code / dictionary scratch must not matter."""
+    import torch
+
+    b = sweep.make_sweep(1024, 1, seed=5)   # plan 0 has ~400 distinct fused values
+    r = sweep.SweepRunner(b)
+    assert all(r.class_coded)
+    a1, t1 = r.run()
+    exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
+    assert np.array_equal(a1, exp_assign)
+    assert [t.hex() for t in t1] == [t.hex() for t in exp_totals]
+    d = r.dict.cpu().numpy()
+    flags = np.concatenate([d[r.dict_off[c] // 8:(r.dict_off[c] + r.dict_need[c]) // 8:256]
+                            for c in range(len(r.classes))])
+    assert len(flags) == b.n_plans
+    assert (flags != -1).sum() >= 1          # some plan overflowed ...
+    assert (flags == -1).sum() >= 1          # ... and some stayed coded
+    r.codes.fill_(0x5A)
+    r.dict.fill_(123)
+    r.fused.fill_(float("nan"))
+    r.perm.fill_(-1)
+    r.upload()
+    r.solve(download=True)
+    torch.cuda.synchronize()
+    a2, t2 = r.results()
+    assert np.array_equal(a1, a2) and [t.hex() for t in t1] == [t.hex() for t in t2]
