@@ -737,11 +737,14 @@ __device__ __forceinline__ void fuse_rows(const sk_plan& p, int q, int bx,
   }
 }
 
+#ifndef SK_FF_MINB
+#define SK_FF_MINB 0  // 0: unspecified (an explicit 1 costs k_fuse 20%: measured 7.61 -> 9.34 ms)
+#endif
 #ifndef SK_FC_MINB
 #define SK_FC_MINB 6
 #endif
 template <int G, int LPG, bool CODES>
-__global__ void __launch_bounds__(kF_TPB, CODES && G <= 4 ? SK_FC_MINB : 1) k_fuse(const sk_plan* __restrict__ plans, int plan0,
+__global__ void __launch_bounds__(kF_TPB, CODES && G <= 4 ? SK_FC_MINB : SK_FF_MINB) k_fuse(const sk_plan* __restrict__ plans, int plan0,
                                                  const int32_t* __restrict__ row_ptr,
                                                  const sk_segment* __restrict__ segs,
                                                  double* __restrict__ F, uint32_t* __restrict__ perm,
@@ -758,35 +761,34 @@ __global__ void __launch_bounds__(kF_TPB, CODES && G <= 4 ? SK_FC_MINB : 1) k_fu
 }
 
 // After a CODES pass: the plans whose fused values overflowed the 255-entry
-// dictionary (its slot 0 set) get their fused rows as doubles, for the outer
-// KM's uncoded path.  A few CTAs walk all plans; the rest exit at the flag.
+// dictionary (its slot 0 set) are listed, then get their fused rows as
+// doubles for the outer KM's uncoded path -- work units (listed plan, row
+// block) spread over a fixed grid, so a few big overflowed plans do not
+// serialise on a few CTAs.
+__global__ void k_overflow_list(const unsigned long long* __restrict__ dict, int n_plans, int* list,
+                                int* count) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n_plans && __ldcg(dict + (size_t)q * kDictSlots) != kEmpty) list[atomicAdd(count, 1)] = q;
+}
+
+constexpr int kF_MAXBX = (4095 + kF_WARPS * 8 - 1) / (kF_WARPS * 8);  // row blocks of a plan (LPG 4)
+
 template <int G>
-__global__ void __launch_bounds__(kF_TPB) k_fuse_overflow(const sk_plan* __restrict__ plans, int n_plans,
+__global__ void __launch_bounds__(kF_TPB) k_fuse_overflow(const sk_plan* __restrict__ plans,
+                                                          const int* __restrict__ list,
+                                                          const int* __restrict__ count,
                                                           const int32_t* __restrict__ row_ptr,
                                                           const sk_segment* __restrict__ segs,
                                                           double* __restrict__ F, uint32_t* __restrict__ perm,
                                                           uint32_t zero_perm, const FuseCodes fc) {
   constexpr int kGroupsPerBlock = kF_WARPS * (32 / 4);
-  __shared__ int s_list[kF_TPB];
-  __shared__ int s_cnt;
-  for (int q0 = blockIdx.x * kF_TPB; q0 < n_plans; q0 += gridDim.x * kF_TPB) {
-    // one flag per thread, the overflowed plans of G listed in shared memory
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    const int q = q0 + threadIdx.x;
-    if (q < n_plans && __ldcg(fc.dict + (size_t)q * kDictSlots) != kEmpty && plans[q].group == G &&
-        !(plans[q].flags & SK_PLAN_GENERIC))
-      s_list[atomicAdd(&s_cnt, 1)] = q;
-    __syncthreads();
-    const int cnt = s_cnt;
-    for (int i = 0; i < cnt; ++i) {
-      const int qq = s_list[i];
-      const sk_plan p = plans[qq];
-      const int nbx = (p.rows / G + kGroupsPerBlock - 1) / kGroupsPerBlock;
-      for (int bx = 0; bx < nbx; ++bx)
-        fuse_rows<G, 4, false>(p, qq, bx, row_ptr, segs, F, perm, zero_perm, fc, nullptr);
-    }
-    __syncthreads();
+  const long long units = (long long)__ldcg(count) * kF_MAXBX;
+  for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    const int q = list[u / kF_MAXBX], bx = (int)(u % kF_MAXBX);
+    const sk_plan p = plans[q];
+    if (p.group != G || (p.flags & SK_PLAN_GENERIC)) continue;
+    if (bx * kGroupsPerBlock >= p.rows / G) continue;
+    fuse_rows<G, 4, false>(p, q, bx, row_ptr, segs, F, perm, zero_perm, fc, nullptr);
   }
 }
 
@@ -853,12 +855,10 @@ int launch_fuse_coded(const sk_plan* d_plans, int p0, int np, int max_n, const i
 }
 
 template <int G>
-int launch_fuse_overflow(const sk_plan* d_plans, int n_plans, const int32_t* row_ptr,
+int launch_fuse_overflow(const sk_plan* d_plans, const int* list, const int* count, const int32_t* row_ptr,
                          const sk_segment* segs, double* F, uint32_t* perm, const FuseCodes& fc,
                          cudaStream_t s) {
-  const int need = (n_plans + kF_TPB - 1) / kF_TPB;
-  const int ctas = need < 148 * 4 ? need : 148 * 4;
-  k_fuse_overflow<G><<<ctas, kF_TPB, 0, s>>>(d_plans, n_plans, row_ptr, segs, F, perm, zero_perm_of(G), fc);
+  k_fuse_overflow<G><<<148 * 4, kF_TPB, 0, s>>>(d_plans, list, count, row_ptr, segs, F, perm, zero_perm_of(G), fc);
   return cuda_check("k_fuse_overflow launch");
 }
 
@@ -1997,7 +1997,8 @@ int64_t sk_precoded_bytes(int n_plans, int max_n, int64_t* dict_bytes) {
   if (n_plans <= 0 || max_n <= 0 || max_n > 4095) return 0;
   int cpl = 0, w = 0;
   outer_shape(max_n, &cpl, &w);
-  if (dict_bytes) *dict_bytes = (int64_t)n_plans * kDictSlots * 8;
+  // the dictionaries, then the overflow list (n_plans ints) and its count
+  if (dict_bytes) *dict_bytes = (int64_t)n_plans * kDictSlots * 8 + 4 * ((int64_t)n_plans + 1);
   return (int64_t)(outer_codes_stride(max_n, w, cpl) * (size_t)n_plans);
 }
 
@@ -2014,7 +2015,11 @@ int sk_map_fuse_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_
     return set_err(SK_EINVAL, "coded fuse: code scratch %lld B / dictionaries %lld B needed (max_n %d)",
                    (long long)need, (long long)need_dict, max_n);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(d_dict, 0xff, (size_t)need_dict, s) != cudaSuccess) return cuda_check("clear dictionaries");
+  const size_t tables = (size_t)n_plans * kDictSlots * 8;
+  int* list = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(d_dict) + tables);
+  int* count = list + n_plans;
+  if (cudaMemsetAsync(d_dict, 0xff, tables, s) != cudaSuccess || cudaMemsetAsync(count, 0, 4, s) != cudaSuccess)
+    return cuda_check("clear dictionaries");
   int cpl = 0, w = 0;
   outer_shape(max_n, &cpl, &w);
   const FuseCodes fc{d_codes, outer_codes_stride(max_n, w, cpl), reinterpret_cast<unsigned long long*>(d_dict)};
@@ -2036,9 +2041,10 @@ int sk_map_fuse_coded(const sk_plan* d_plans, int n_plans, const int32_t* d_row_
 #undef SK_FUSE_CODED
     if (rc) return rc;
   }
-  int rc = SK_OK;
+  k_overflow_list<<<(n_plans + 255) / 256, 256, 0, s>>>(fc.dict, n_plans, list, count);
+  int rc = cuda_check("k_overflow_list launch");
 #define SK_FUSE_OVF(GG) \
-  if (!rc && (mask & (1 << GG))) rc = launch_fuse_overflow<GG>(d_plans, n_plans, d_row_ptr, d_segs, d_fused, d_perm, fc, s);
+  if (!rc && (mask & (1 << GG))) rc = launch_fuse_overflow<GG>(d_plans, list, count, d_row_ptr, d_segs, d_fused, d_perm, fc, s);
   SK_FUSE_OVF(1) SK_FUSE_OVF(2) SK_FUSE_OVF(3) SK_FUSE_OVF(4)
   SK_FUSE_OVF(5) SK_FUSE_OVF(6) SK_FUSE_OVF(7) SK_FUSE_OVF(8)
 #undef SK_FUSE_OVF

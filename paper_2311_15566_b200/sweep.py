@@ -254,7 +254,7 @@ class SweepRunner:
             pc = int(self.lib.sk_precoded_bytes(b - a, mn, ctypes.byref(d))) if self.precoded else 0
             coded.append(pc > 0)
             need.append(pc if pc > 0 else int(self.lib.sk_outer_codes_bytes(b - a, mn, rows)))
-            dneed.append(int(d.value) if pc > 0 else 0)
+            dneed.append(_align(int(d.value)) if pc > 0 else 0)
         self.class_coded = coded
         self.codes_off = np.concatenate([[0], np.cumsum(need)]).astype(np.int64)
         self.codes_need = need

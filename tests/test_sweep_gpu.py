@@ -137,8 +137,8 @@ def test_coded_fuse_overflow_and_stale_scratch():
     assert np.array_equal(a1, exp_assign)
     assert [t.hex() for t in t1] == [t.hex() for t in exp_totals]
     d = r.dict.cpu().numpy()
-    flags = np.concatenate([d[r.dict_off[c] // 8:(r.dict_off[c] + r.dict_need[c]) // 8:256]
-                            for c in range(len(r.classes))])
+    flags = np.concatenate([d[r.dict_off[c] // 8:r.dict_off[c] // 8 + 256 * (hi - lo):256]
+                            for c, (lo, hi, _) in enumerate(r.classes)])
     assert len(flags) == b.n_plans
     assert (flags != -1).sum() >= 1          # some plan overflowed ...
     assert (flags == -1).sum() >= 1          # ... and some stayed coded
