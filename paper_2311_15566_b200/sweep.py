@@ -244,14 +244,19 @@ class SweepRunner:
                            for a, b, _ in self.classes]
         # global code scratch for the big size classes (sk_outer_codes_bytes);
         # the classes run concurrently, so each gets its own slice
-        # coded K2 (default; SK_PRECODED=0 disables, for A/B): k_fuse writes
-        # one-byte codes + a per-plan dictionary instead of the double matrix,
-        # so every codable class needs the code scratch and dictionaries
-        self.precoded = os.environ.get("SK_PRECODED", "1") != "0"
+        # coded K2: k_fuse writes one-byte codes + a per-plan dictionary instead
+        # of the double matrix (every codable class then needs the code scratch
+        # and dictionaries) -- for sweeps whose largest outer problem has n >= 96 (measured per
+        # sweep size, all classes coded vs none: -6% at 64 positions (n <= 38),
+        # -2% at 128 (n <= 70), +4% at 256, +7.5% at 512, +5% at 1,024; per-class
+        # mixes measured no better).  SK_PRECODED=0 / 1 forces it off / on.
+        mode = os.environ.get("SK_PRECODED", "auto")
+        self.precoded = mode == "1" or (mode != "0" and self.max_n >= 96)
         need, dneed, coded = [], [], []
         for (a, b, mn), rows in zip(self.classes, self.class_rows):
             d = ctypes.c_int64(0)
-            pc = int(self.lib.sk_precoded_bytes(b - a, mn, ctypes.byref(d))) if self.precoded else 0
+            use = self.precoded
+            pc = int(self.lib.sk_precoded_bytes(b - a, mn, ctypes.byref(d))) if use else 0
             coded.append(pc > 0)
             need.append(pc if pc > 0 else int(self.lib.sk_outer_codes_bytes(b - a, mn, rows)))
             dneed.append(_align(int(d.value)) if pc > 0 else 0)

@@ -151,3 +151,17 @@ def test_coded_fuse_overflow_and_stale_scratch():
     torch.cuda.synchronize()
     a2, t2 = r.results()
     assert np.array_equal(a1, a2) and [t.hex() for t in t1] == [t.hex() for t in t2]
+
+
+@pytest.mark.parametrize("n_pos,fused_sum", [(64, False), (128, False), (128, True)])
+def test_coded_path_forced_at_small_sizes(monkeypatch, n_pos, fused_sum):
+    """The coded K2 runs by default from n >= 96; forced on, the small sweeps
+    must give the same bits as the C oracle too."""
+    monkeypatch.setenv("SK_PRECODED", "1")
+    b = sweep.make_sweep(n_pos, 2, seed=11 + n_pos, fused_sum=fused_sum)
+    r = sweep.SweepRunner(b)
+    assert all(r.class_coded)
+    assign, totals = r.run()
+    exp_assign, exp_totals = cport.map_sweep(b.desc, b.plans, b.alive, b.tok)
+    assert np.array_equal(assign, exp_assign)
+    assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
