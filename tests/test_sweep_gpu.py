@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("n_pos,sets,fused_sum,model", [
     (64, 4, False, "gpt-20b"), (128, 2, False, "gpt-20b"), (256, 2, False, "gpt-20b"),
     (512, 1, False, "gpt-20b"), (1024, 1, False, "gpt-20b"), (128, 2, True, "gpt-20b"),
-    (256, 1, False, "llama-30b"), (64, 2, False, "opt-6.7b"),
+    (256, 1, False, "llama-30b"), (64, 2, False, "opt-6.7b"), (256, 1, True, "gpt-20b"),
+    (256, 1, False, "opt-6.7b"),
 ])
 def test_sweep_matches_c_oracle(n_pos, sets, fused_sum, model):
     geom, shapes = sweep.MODELS[model]
