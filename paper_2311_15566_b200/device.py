@@ -9,6 +9,9 @@ PyTorch provides device memory and the stream; all compute is libspotkm.so.
 
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 import torch
 
@@ -129,15 +132,48 @@ class MapBatch:
         p_total = out.data_ptr()
         p_assign = p_total + 8 * Q
         st = _stream_ptr()
-        rc = lib.sk_map_fuse(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
-                             info["max_na"], info["max_nb"], info["gmask"], 0, 0, st)
-        nat.check(rc, mapping_error)
         ns = np.array([n_of[q] for q in order], dtype=np.int64)
-        for a, b, mn in outer_classes(ns):
-            mr = int(plans["rows"][a:b].max())
-            rc = lib.sk_map_outer(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
-                                  perm.data_ptr(), p_assign, p_total + 8 * a, 0, mn, mr, st)
+        if os.environ.get("SK_PRECODED", "0") == "1":
+            # the sweep's coded K2 per size class (opt-in for the drop-in: its
+            # calls are small, where the double matrix measured faster)
+            g = plans["group"].astype(np.int64)
+            na = plans["rows"].astype(np.int64) // g
+            nb = (plans["D"] * plans["P"] * plans["M"]).astype(np.int64) // g
+            gbit = np.where(plans["flags"] & nat.SK_PLAN_GENERIC, 1, np.left_shift(1, g))
+            keep = []
+            for a, b, mn in outer_classes(ns):
+                mr = int(plans["rows"][a:b].max())
+                d = ctypes.c_int64(0)
+                cb = int(lib.sk_precoded_bytes(b - a, mn, ctypes.byref(d)))
+                cmask = int(np.bitwise_or.reduce(gbit[a:b]))
+                if cb > 0:
+                    codes = torch.empty(cb, dtype=torch.uint8, device=dev)
+                    dct = torch.empty((int(d.value) + 7) // 8, dtype=torch.int64, device=dev)
+                    keep += [codes, dct]
+                    rc = lib.sk_map_fuse_coded(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                               perm.data_ptr(), int(na[a:b].max()), int(nb[a:b].max()),
+                                               cmask, codes.data_ptr(), cb, dct.data_ptr(), int(d.value), st)
+                    nat.check(rc, mapping_error)
+                    rc = lib.sk_map_outer_coded(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                                perm.data_ptr(), p_assign, p_total + 8 * a, 0, mn, mr,
+                                                codes.data_ptr(), cb, dct.data_ptr(), st)
+                else:
+                    rc = lib.sk_map_fuse(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                         perm.data_ptr(), int(na[a:b].max()), int(nb[a:b].max()), cmask,
+                                         0, 0, st)
+                    nat.check(rc, mapping_error)
+                    rc = lib.sk_map_outer(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                          perm.data_ptr(), p_assign, p_total + 8 * a, 0, mn, mr, st)
+                nat.check(rc, mapping_error)
+        else:
+            rc = lib.sk_map_fuse(p_plans, Q, p_rp, p_segs, fused.data_ptr(), perm.data_ptr(),
+                                 info["max_na"], info["max_nb"], info["gmask"], 0, 0, st)
             nat.check(rc, mapping_error)
+            for a, b, mn in outer_classes(ns):
+                mr = int(plans["rows"][a:b].max())
+                rc = lib.sk_map_outer(p_plans + 64 * a, b - a, p_rp, p_segs, fused.data_ptr(),
+                                      perm.data_ptr(), p_assign, p_total + 8 * a, 0, mn, mr, st)
+                nat.check(rc, mapping_error)
         host = out.cpu().numpy().view(np.uint8)
         del dev_in
         totals_sorted = host[:8 * Q].view(np.float64)

@@ -57,8 +57,11 @@ def test_map_devices_golden_r2(golden, name):
     assert n >= 30
 
 
-def test_generic_plans_batched_with_regular_ones(golden):
-    """general-range and regular plans in ONE device batch"""
+@pytest.mark.parametrize("coded", ["0", "1"])
+def test_generic_plans_batched_with_regular_ones(golden, monkeypatch, coded):
+    """general-range and regular plans in ONE device batch (coded = 1: the
+    coded K2 entry points, general-range plans keeping their double matrix)"""
+    monkeypatch.setenv("SK_PRECODED", coded)
     cases = golden("edge")["cases"] + golden("mapping")["cases"][:40]
     cases = [c for c in cases if not c["error"]]
     probs = [own_problem(c) for c in cases]
@@ -102,7 +105,9 @@ def test_sweep_beyond_4095_outer_vs_c_oracle():
     assert [t.hex() for t in totals] == [t.hex() for t in exp_totals]
 
 
-def test_headline_sweep_plans_vs_reference(golden):
+@pytest.mark.parametrize("coded", ["auto", "1"])
+def test_headline_sweep_plans_vs_reference(golden, monkeypatch, coded):
+    monkeypatch.setenv("SK_PRECODED", coded)
     cases = golden("sweep_ref")["cases"]
     by_n = {}
     for c in cases:
