@@ -1,18 +1,20 @@
 #!/usr/bin/env python
 """Benchmark: batched device-mapping sweep (BASELINE.json configs[2]).
 
-One "step" = one pass of the hot path (sk_sweep_expand -> sk_map_fuse ->
-sk_map_outer) over one batch of synthetic sweep plans: every (old, new)
-GPT-20B candidate config pair at N target positions x S preemption sets.
+One "step" = one pass of the hot path (sk_sweep_expand -> per size class
+sk_map_fuse_coded -> sk_map_outer_coded; the double-matrix sk_map_fuse ->
+sk_map_outer for sweeps with outer n < 96) over one batch of synthetic sweep
+plans: every (old, new) GPT-20B candidate config pair at N target positions x
+S preemption sets.
 
   value  plans/s with inputs resident in HBM (device-timed, CUDA events on
          the launching stream, L2 flushed between steps), max over ranks
   e2e    same metric through the public batched API (SweepRunner): pinned
          H2D of the compact plan descriptors + kernels + D2H of assignments
          and total weights, every step
-  --impl reference   the reference's CPU algorithm (oracle/port.py, a
-         restatement of spotsim's map_devices measured within ~10% of the
-         reference's own speed) on all host cores, rank 0 only
+  --impl reference   the unmodified reference (spotsim.map_devices from
+         baseline/_ref; oracle/port.py only if that install is absent) on all
+         host cores, rank 0 only
 
 Multi-GPU (torchrun): plans are independent, so each rank solves its own
 batch (no data-path collective; weak scaling); times are maxed over ranks.
@@ -583,15 +585,23 @@ def run_ours(args):
     nA, nB = stats["nA"], stats["nB"]
     # algorithmic HBM bytes per launch-set (per step):
     #   k_sweep_expand: writes 2 segments (64 B) + row_ptr (4 B) per row, reads descriptors
-    #   k_fuse: reads 2 segments per row once + writes fused weight (8 B) + perm (4 B) per pair
-    #   k_outer: reads the fused matrix once (8 B per pair), writes assign + total
+    #   k_fuse: reads 2 segments per row once + writes the fused weight (8 B; coded: a 1 B
+    #     code per padded n x n entry + the 2 KB dictionary) + perm (4 B) per pair
+    #   k_outer: reads the fused matrix once (8 B per pair; coded: 1 B per padded entry +
+    #     the dictionary), the epilogue's segments (64 B per row), writes assign + total
+    pairs = float(stats["pairs"].sum())
+    if runner.precoded:
+        padded = float((stats["n"].astype(np.float64) ** 2).sum())
+        fuse_b = padded + 4 * pairs + 64 * batch.rows + 2048 * batch.n_plans
+        outer_b = padded + 2048 * batch.n_plans + 68 * batch.rows + 8 * batch.n_plans
+    else:
+        fuse_b = 12 * pairs + 64 * batch.rows
+        outer_b = 8 * pairs + 68 * batch.rows + 8 * batch.n_plans
     kernels = {
         "k_sweep_expand": {"ms": kms.get("k_sweep_expand", 0.0),
                            "bytes": int(68 * batch.rows + 112 * batch.n_plans)},
-        "k_fuse": {"ms": kms.get("k_fuse", 0.0),
-                   "bytes": int(12 * stats["pairs"].sum() + 64 * batch.rows)},
-        "k_outer": {"ms": kms.get("k_outer", 0.0),
-                    "bytes": int(8 * stats["pairs"].sum() + 4 * batch.rows + 8 * batch.n_plans)},
+        "k_fuse": {"ms": kms.get("k_fuse", 0.0), "bytes": int(fuse_b)},
+        "k_outer": {"ms": kms.get("k_outer", 0.0), "bytes": int(outer_b)},
     }
     dom = max(kernels, key=lambda k: kernels[k]["ms"])
     pk, src = peaks()

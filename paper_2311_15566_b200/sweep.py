@@ -277,11 +277,15 @@ class SweepRunner:
     @property
     def launches_per_solve(self) -> int:
         """Kernel launches of one solve(): expand and fuse split the plans into
-        chunks of at most 65,535 (grid y); one fuse launch per group size."""
+        chunks of at most 65,535 (grid y); one fuse launch per group size; a
+        coded class adds the overflow list and one overflow re-fuse per regular
+        group size."""
         ch = lambda q: -(-q // 65535)  # noqa: E731
         n = 0 if self.expand_per_class else ch(self.b.n_plans)
-        for (a, b, _), m in zip(self.classes, self.class_gmask):
+        for (a, b, _), m, coded in zip(self.classes, self.class_gmask, self.class_coded):
             n += bin(m).count("1") * ch(b - a) + 1 + (ch(b - a) if self.expand_per_class else 0)
+            if coded:
+                n += 1 + bin(m & 0x1fe).count("1")
         return n
 
     def _s(self) -> int:
