@@ -139,12 +139,28 @@ __device__ __forceinline__ double weight_generic(const sk_plan& p, const int32_t
   return sk_exact::rat_to_double(acc, p.Kw);
 }
 
+// one 32-byte segment as two 16-byte loads (one L2 request per segment
+// instead of one per field when the threads of a warp read different rows)
+__device__ __forceinline__ sk_segment load_seg(const sk_segment* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 u = __ldg(q), v = __ldg(q + 1);
+  sk_segment s;
+  s.l0 = u.x;
+  s.l1 = u.y;
+  s.a = u.z;
+  s.b = u.w;
+  s.pipe = v.x;
+  s.reserved = v.y;
+  s.unit = (long long)(((unsigned long long)(unsigned)v.w << 32) | (unsigned)v.z);
+  return s;
+}
+
 __device__ __forceinline__ double weight_at(const sk_plan& p, const int32_t* __restrict__ row_ptr,
                                             const sk_segment* __restrict__ segs, int r, int c) {
   const Col col = col_of(p, c);
   const int s0 = row_ptr[p.row_base + r], s1 = row_ptr[p.row_base + r + 1];
   long long acc = 0;
-  for (int s = s0; s < s1; ++s) acc += seg_num(segs[s], col);
+  for (int s = s0; s < s1; ++s) acc += seg_num(load_seg(segs + s), col);
   return num_to_w(acc, p.K);
 }
 
